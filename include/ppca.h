@@ -1,0 +1,190 @@
+/*
+ * ppca.h — C ABI of the B200-native primed-PCA (pPCA) hot path (arXiv 2109.03709).
+ *
+ * The problem statement is Algorithm 1 of the paper: a centred dataset
+ * X ∈ R^{n×d} (L14), parameters k, l and a PRIMING method in; the first k principal
+ * directions (eigenvectors of XᵀX, L15) and their eigenvalue estimates out.  PRIMING
+ * runs on m = k + l directions (§3.3 "Extra components", L111-114).
+ *
+ * Conventions (all entry points):
+ *  - Vector sets are [m][d] row-major float32 device arrays: row i is the d-vector v_i
+ *    ("ordered list of d-vectors").  X is row-major [n_local][ld] (float32 or bf16).
+ *  - Ownership: the caller allocates every device buffer it passes (X, W, V, velocity, E, T)
+ *    and every host output; the library never frees caller memory.  The context owns its
+ *    NCCL communicator, its events and a grow-only device scratch pool.
+ *  - Streams: all work is enqueued on the context's stream.  Each call synchronises that
+ *    stream once before returning, so it can report a status; no host sync happens inside
+ *    an iteration loop.
+ *  - Collectives: with world > 1 every call is collective (like NCCL): all ranks call it with
+ *    the same arguments except their own X shard; results (W, E, θ) are bitwise identical on
+ *    all ranks.  The only collective is an NCCL all-reduce (sum) of per-rank partial products.
+ *  - Errors: a non-OK status leaves outputs unspecified.  ppca_last_error() returns a message.
+ *  - Numerics: X in fp32 or bf16; products accumulated in fp32 (hybrid fp32/fp64 for long
+ *    reductions), every m×m quantity (Gram, Cholesky, Jacobi) in fp64.
+ */
+#ifndef PPCA_H
+#define PPCA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPCA_ABI_VERSION 1
+#define PPCA_UNIQUE_ID_BYTES 128   /* sizeof(ncclUniqueId) */
+#define PPCA_MAX_M 128             /* largest supported m = k + l */
+
+typedef enum {
+  PPCA_OK = 0,
+  PPCA_ERR_INVALID_ARG = 1,          /* null pointer, bad enum, k > m, ld*elt % 16 != 0 ... */
+  PPCA_ERR_DIM_MISMATCH = 2,
+  PPCA_ERR_TOO_MANY_COMPONENTS = 3,  /* m > d or m > PPCA_MAX_M */
+  PPCA_ERR_NONFINITE = 4,            /* a priming update produced Inf/NaN */
+  PPCA_ERR_DEGENERATE = 5,           /* EigenGame v_iᵀMv_i <= 1e-12·max, zero vector (L225) */
+  PPCA_ERR_SUBSPACE_COLLAPSE = 6,    /* orthonormalisation lost rank / fewer than k survive */
+  PPCA_ERR_NO_CONVERGENCE = 7,       /* Jacobi exceeded 100 sweeps */
+  PPCA_ERR_CUDA = 8,
+  PPCA_ERR_NCCL = 9,
+  PPCA_ERR_UNSUPPORTED = 10          /* not an sm_100 device, NCCL missing for world > 1, ... */
+} ppca_status;
+
+typedef enum { PPCA_F32 = 0, PPCA_BF16 = 1 } ppca_dtype;
+
+/* Row layout of a shard.  CONTIGUOUS: rank g holds global rows [⌈n/G⌉g, ⌈n/G⌉(g+1)).
+ * INTERLEAVED: every minibatch block of block_rows rows (the last one may be shorter, size p)
+ * is split in G equal slices; rank g holds rows [s·b + g·p/G, s·b + (g+1)·p/G) of block s,
+ * so a global minibatch is identical for every G (reading R10). */
+typedef enum { PPCA_LAYOUT_CONTIGUOUS = 0, PPCA_LAYOUT_INTERLEAVED = 1 } ppca_layout;
+
+typedef enum { PPCA_PLANTED_QR = 0, PPCA_PLANTED_HOUSEHOLDER = 1, PPCA_IMAGE_FACTOR = 2 } ppca_family;
+typedef enum { PPCA_SPECTRUM_EXP = 0, PPCA_SPECTRUM_POWER = 1 } ppca_spectrum;
+
+typedef struct ppca_ctx ppca_ctx;
+
+/* This rank's row shard of the centred X. */
+typedef struct {
+  const void* data;     /* device, row-major [n_local][ld] of dtype */
+  ppca_dtype dtype;
+  int64_t n_local;      /* rows stored on this rank (may be 0) */
+  int64_t n_global;     /* rows over all ranks */
+  int64_t d;            /* dimension */
+  int64_t ld;           /* row stride in elements, ld >= d, ld*sizeof(dtype) % 16 == 0 */
+  ppca_layout layout;
+  int64_t block_rows;   /* minibatch block b for INTERLEAVED (0 otherwise) */
+} ppca_matrix;
+
+/* Synthetic generator (BASELINE.json configs[0..4]). */
+typedef struct {
+  ppca_family family;
+  ppca_spectrum spectrum;  /* EXP: λ_j = exp(-j/a); POWER: λ_j = j^-a; j = 1..d */
+  double a;
+  double noise;            /* added to every λ_j */
+  int32_t relu;            /* planted_householder: max(0, ·) */
+  int32_t house_r;         /* number of Householder reflections */
+  int32_t rank;            /* image_factor inner dimension (50) */
+  ppca_dtype dtype;        /* storage */
+  int64_t n_global;
+  int64_t d;
+  uint64_t seed;
+  ppca_layout layout;
+  int64_t block_rows;
+} ppca_gen_spec;
+
+/* ---------------------------------------------------------------- context */
+const char* ppca_status_string(ppca_status s);
+int ppca_abi_version(void);
+
+/* NCCL unique id for a world > 1 context (rank 0 calls it and broadcasts the bytes).
+ * uid_out: host buffer of PPCA_UNIQUE_ID_BYTES. */
+ppca_status ppca_get_unique_id(void* uid_out);
+
+/* device: CUDA ordinal; stream: cudaStream_t or NULL (legacy default stream);
+ * uid: PPCA_UNIQUE_ID_BYTES host bytes (required if world > 1, ignored otherwise). */
+ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank, int world,
+                            ppca_ctx** out);
+ppca_status ppca_ctx_destroy(ppca_ctx* ctx);
+/* Copies the last error message of ctx (NUL-terminated, truncated to cap). */
+ppca_status ppca_last_error(const ppca_ctx* ctx, char* msg, size_t cap);
+/* Number of library kernel launches enqueued by this context since creation (bench evidence). */
+int64_t ppca_launch_count(const ppca_ctx* ctx);
+
+/* ---------------------------------------------------------------- hot path */
+
+/* Writes this rank's shard of the seeded synthetic X (centred by the fp64 mean over all
+ * n_global rows, rounded to spec->dtype) into the caller's device buffer X [n_local][ld].
+ * n_local_out: rows written; col_mean_host: optional host double[d] receiving the mean. */
+ppca_status ppca_generate(ppca_ctx* ctx, const ppca_gen_spec* spec, void* X, int64_t ld,
+                          int64_t* n_local_out, double* col_mean_host);
+
+/* Block power priming (§2.1, multi-component by re-orthonormalisation L63):
+ * per iteration Y = X·Wᵀ, Z = YᵀX (fused streaming pass over X), all-reduce, W ← orth(Z)
+ * (Q-factor with positive diag R).  W: device [m][d] in/out.  init_seed != 0 initialises W
+ * from N(0,1) draws (Philox stream 6) then orthonormalises; init_seed == 0 resumes from W.
+ * theta_hist_host: optional host double[iters*m]: row t holds the pPCA (Rayleigh–Ritz)
+ * eigenvalue estimates of span(W_t) computed from the same pass (S_t = YᵀY), descending. */
+ppca_status ppca_prime_power(ppca_ctx* ctx, const ppca_matrix* X, int m, int iters,
+                             uint64_t init_seed, float* W, double* theta_hist_host);
+
+/* Generalised Oja / Sanger minibatch priming (§2.2; Nesterov L326):
+ * G = X_bᵀY_b − W·triu(Y_bᵀY_b) summed over the global minibatch (reading R8), v ← μv + G,
+ * W ← W + α(G + μv).  Minibatch s uses global block s mod ⌈n/b⌉ (reading R10).
+ * W, velocity: device [m][d] in/out; step_io: in = first global step, out = next step.
+ * init_seed != 0 initialises W (unit N(0,1) rows) and zeroes velocity. */
+ppca_status ppca_prime_oja(ppca_ctx* ctx, const ppca_matrix* X, int m, int batch, double alpha,
+                           double momentum, int64_t steps, uint64_t init_seed, float* W,
+                           float* velocity, int64_t* step_io);
+
+/* α-EigenGame minibatch priming (§2.3 Eqs. 1-3; update rule reading R11):
+ * ∇_j = 2M_b v_j − 2Σ_{i<j}(v_jᵀM_b v_i / v_iᵀM_b v_i) M_b v_i, tangent projection,
+ * Nesterov, renormalisation.  Same argument conventions as ppca_prime_oja (V in/out). */
+ppca_status ppca_prime_eigengame(ppca_ctx* ctx, const ppca_matrix* X, int m, int batch,
+                                 double alpha, double momentum, int64_t steps,
+                                 uint64_t init_seed, float* V, float* velocity,
+                                 int64_t* step_io);
+
+/* pPCA refinement, Algorithm 1 steps 2-5: B = orth(V); S = (XBᵀ)ᵀ(XBᵀ)
+ * (projected covariance, never forming π_S(x)); (θ, U) = eig(S) in fp64 (generalised with
+ * the Gram of the operand actually used); E = U_kᵀB with the sign convention (largest-|entry|
+ * positive).  V: device [m][d]; E: device [k][d] out; theta_host: host double[k] out
+ * (eigenvalues of XᵀX restricted to span V, unnormalised, descending); subspace_dim: out. */
+ppca_status ppca_refine(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k,
+                        float* E, double* theta_host, int* subspace_dim);
+
+/* Evaluation (§5.3): angle_i = arccos(min(1,|<E_i,T_i>|)) and
+ * LCES(V) = #consecutive i from 1 with angle_i < V (strict), for each threshold.
+ * E, T: device [k][d] unit rows.  angles_host: double[k]; lces_host: int[nthr]. */
+ppca_status ppca_eval(ppca_ctx* ctx, const float* E, const float* T, int k, int64_t d,
+                      const double* thr_host, int nthr, double* angles_host, int* lces_host);
+
+/* Captured variance vᵀ(XᵀX)v = ‖Xv‖² for each row of V (PAPER.md L416 footnote),
+ * summed over ranks.  var_host: double[m]. */
+ppca_status ppca_captured_variance(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m,
+                                   double* var_host);
+
+/* Support (ground truth for evaluation, untimed): G = XᵀX in fp64, device double[d][d],
+ * summed over ranks. */
+ppca_status ppca_gram(ppca_ctx* ctx, const ppca_matrix* X, double* G);
+
+/* Support (generator parity tests): Philox4x32-10 words w[e], e in [first, first+count) of
+ * (seed, stream) into device uint32 out[count] (DESIGN.md §Inputs counter convention). */
+ppca_status ppca_philox_words(ppca_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t first,
+                              int64_t count, uint32_t* out);
+
+/* Timing hook (bench.py): with enable != 0, every streaming pass over X (power or refine
+ * mode) is bracketed by CUDA events on the context stream.  ppca_get_pass_time returns the
+ * summed device time (ms) and the number of passes recorded since the last call, then resets. */
+ppca_status ppca_set_timing(ppca_ctx* ctx, int enable);
+ppca_status ppca_get_pass_time(ppca_ctx* ctx, double* ms_total, int64_t* passes);
+
+/* Timing hook: select the fused-pass implementation (0 = auto, 1 = SIMT fp32, 2 = tcgen05).
+ * Returns UNSUPPORTED if the requested path cannot run this matrix. */
+ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);
+/* Implementation used by the most recent pass (1 = SIMT, 2 = tcgen05; 0 = none yet). */
+int ppca_last_pass_impl(const ppca_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPCA_H */

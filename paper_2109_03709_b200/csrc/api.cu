@@ -1,0 +1,511 @@
+// api.cu — the C ABI (include/ppca.h): context, NCCL plumbing, and the hot-path drivers.
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <math.h>
+#include <algorithm>
+#include <nccl.h>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "small.cuh"
+#include "pass.cuh"
+
+struct ppca_ctx {
+  ppca::Ctx c;
+};
+
+namespace ppca {
+
+ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_t* n_local_out, double* mu_host);
+ppca_status philox_words(Ctx* c, uint64_t seed, uint32_t stream, uint64_t first, int64_t count, uint32_t* out);
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+
+static bool nccl_load() {
+  if (g_nccl.loaded) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+  return g_nccl.loaded;
+}
+
+// ----------------------------------------------------------------------------- errors / scratch
+ppca_status set_error(Ctx* c, ppca_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->last_error = buf;
+  return s;
+}
+
+ppca_status check_cuda(Ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PPCA_OK;
+  return set_error(c, PPCA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void* scratch(Ctx* c, int slot, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (c->slot_bytes[slot] >= bytes) return c->slot_ptr[slot];
+  if (c->slot_ptr[slot]) {
+    cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);
+    cudaFree(c->slot_ptr[slot]);
+    c->slot_ptr[slot] = nullptr;
+    c->slot_bytes[slot] = 0;
+  }
+  size_t want = bytes + bytes / 4;
+  void* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    want = bytes;
+  }
+  c->slot_ptr[slot] = p;
+  c->slot_bytes[slot] = want;
+  return p;
+}
+
+ppca_status finish(Ctx* c, const char* what) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && c->side) e = cudaStreamSynchronize(c->side);
+  if (e != cudaSuccess) return check_cuda(c, e, what);
+  int h = 0;
+  e = cudaMemcpy(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return check_cuda(c, e, what);
+  if (h) cudaMemset(c->d_err, 0, sizeof(int));
+  if (h & DEV_NONFINITE) return set_error(c, PPCA_ERR_NONFINITE, "%s: non-finite update", what);
+  if (h & DEV_DEGENERATE) return set_error(c, PPCA_ERR_DEGENERATE, "%s: degenerate denominator / zero vector", what);
+  if (h & DEV_COLLAPSE) return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "%s: orthonormalisation lost rank", what);
+  if (h & DEV_NOCONV) return set_error(c, PPCA_ERR_NO_CONVERGENCE, "%s: Jacobi exceeded 100 sweeps", what);
+  return PPCA_OK;
+}
+
+ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64) {
+  if (c->world <= 1 || count == 0) return PPCA_OK;
+  ncclResult_t r = g_nccl.AllReduce(buf, buf, count, f64 ? ncclFloat64 : ncclFloat32, ncclSum,
+                                    (ncclComm_t)c->nccl_comm, c->stream);
+  if (r != ncclSuccess) return set_error(c, PPCA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+  return PPCA_OK;
+}
+
+// ----------------------------------------------------------------------------- validation
+static ppca_status check_matrix(Ctx* c, const ppca_matrix* X, int m) {
+  if (!X || (!X->data && X->n_local > 0)) return set_error(c, PPCA_ERR_INVALID_ARG, "null matrix");
+  if (X->d < 1 || X->ld < X->d || X->n_local < 0 || X->n_global < X->n_local)
+    return set_error(c, PPCA_ERR_DIM_MISMATCH, "bad matrix dims n_local=%lld d=%lld ld=%lld", (long long)X->n_local,
+                     (long long)X->d, (long long)X->ld);
+  if (X->dtype != PPCA_F32 && X->dtype != PPCA_BF16) return set_error(c, PPCA_ERR_INVALID_ARG, "bad dtype");
+  if ((X->ld * (int64_t)elt_size(X->dtype)) % 16) return set_error(c, PPCA_ERR_INVALID_ARG, "ld*elt %% 16 != 0");
+  if (m < 1) return set_error(c, PPCA_ERR_INVALID_ARG, "m must be >= 1");
+  if (m > PPCA_MAX_M || m > X->d)
+    return set_error(c, PPCA_ERR_TOO_MANY_COMPONENTS, "m=%d exceeds d=%lld or %d", m, (long long)X->d, PPCA_MAX_M);
+  return PPCA_OK;
+}
+
+// local row range of global minibatch block s (reading R10)
+static void block_range(const ppca_matrix* X, int world, int64_t b, int64_t s, int64_t* r0, int64_t* rows) {
+  int64_t n = X->n_global, nb = ceil_div(n, b), nbf = n / b;
+  s %= nb;
+  int64_t q = b / world;
+  if (s < nbf) {
+    *r0 = s * q;
+    *rows = q;
+  } else {
+    *r0 = nbf * q;
+    *rows = (n - nbf * b) / world;
+  }
+}
+
+}  // namespace ppca
+
+using namespace ppca;
+
+// ============================================================================= ABI
+extern "C" {
+
+const char* ppca_status_string(ppca_status s) {
+  switch (s) {
+    case PPCA_OK: return "ok";
+    case PPCA_ERR_INVALID_ARG: return "invalid argument";
+    case PPCA_ERR_DIM_MISMATCH: return "dimension mismatch";
+    case PPCA_ERR_TOO_MANY_COMPONENTS: return "too many components";
+    case PPCA_ERR_NONFINITE: return "non-finite update";
+    case PPCA_ERR_DEGENERATE: return "degenerate denominator";
+    case PPCA_ERR_SUBSPACE_COLLAPSE: return "subspace collapse";
+    case PPCA_ERR_NO_CONVERGENCE: return "no convergence";
+    case PPCA_ERR_CUDA: return "CUDA error";
+    case PPCA_ERR_NCCL: return "NCCL error";
+    case PPCA_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+int ppca_abi_version(void) { return PPCA_ABI_VERSION; }
+
+ppca_status ppca_get_unique_id(void* uid_out) {
+  if (!uid_out) return PPCA_ERR_INVALID_ARG;
+  if (!nccl_load()) return PPCA_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return PPCA_ERR_NCCL;
+  memcpy(uid_out, &id, sizeof(id));
+  return PPCA_OK;
+}
+
+ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank, int world, ppca_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return PPCA_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return PPCA_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return PPCA_ERR_CUDA;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10) return PPCA_ERR_UNSUPPORTED;   // sm_100a build
+  ppca_ctx* h = new ppca_ctx();
+  Ctx* c = &h->c;
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->sm_count = prop.multiProcessorCount;
+  c->stream = (cudaStream_t)stream;
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) {
+    delete h;
+    return PPCA_ERR_CUDA;
+  }
+  if (world > 1) {
+    if (!uid) { delete h; return PPCA_ERR_INVALID_ARG; }
+    if (!nccl_load()) { delete h; return PPCA_ERR_UNSUPPORTED; }
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    ncclComm_t comm;
+    if (g_nccl.CommInitRank(&comm, world, id, rank) != ncclSuccess) { delete h; return PPCA_ERR_NCCL; }
+    c->nccl_comm = comm;
+  }
+  *out = h;
+  return PPCA_OK;
+}
+
+ppca_status ppca_ctx_destroy(ppca_ctx* h) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->side) cudaStreamSynchronize(c->side);
+  for (int i = 0; i < Ctx::kSlots; ++i)
+    if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  if (c->d_err) cudaFree(c->d_err);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->nccl_comm) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
+  pass_release(c);
+  delete h;
+  return PPCA_OK;
+}
+
+ppca_status ppca_last_error(const ppca_ctx* h, char* msg, size_t cap) {
+  if (!h || !msg || cap == 0) return PPCA_ERR_INVALID_ARG;
+  snprintf(msg, cap, "%s", h->c.last_error.c_str());
+  return PPCA_OK;
+}
+
+int64_t ppca_launch_count(const ppca_ctx* h) { return h ? h->c.launches : -1; }
+
+ppca_status ppca_set_timing(ppca_ctx* h, int enable) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  h->c.timing = enable != 0;
+  h->c.tev_used = 0;
+  return PPCA_OK;
+}
+
+ppca_status ppca_get_pass_time(ppca_ctx* h, double* ms_total, int64_t* passes) {
+  if (!h || !ms_total || !passes) return PPCA_ERR_INVALID_ARG;
+  cudaSetDevice(h->c.device);
+  return pass_time_collect(&h->c, ms_total, passes);
+}
+
+int ppca_last_pass_impl(const ppca_ctx* h) { return h ? h->c.last_impl : -1; }
+
+ppca_status ppca_set_pass_impl(ppca_ctx* h, int impl) {
+  if (!h || impl < 0 || impl > 2) return PPCA_ERR_INVALID_ARG;
+  h->c.pass_impl = impl;
+  return PPCA_OK;
+}
+
+ppca_status ppca_generate(ppca_ctx* h, const ppca_gen_spec* spec, void* X, int64_t ld, int64_t* n_local_out,
+                          double* col_mean_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(generate(c, spec, X, ld, n_local_out, col_mean_host));
+  return finish(c, "ppca_generate");
+}
+
+ppca_status ppca_philox_words(ppca_ctx* h, uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
+                              uint32_t* out) {
+  if (!h || (!out && count > 0)) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(philox_words(c, seed, stream, first, count, out));
+  return finish(c, "ppca_philox_words");
+}
+
+// ---------------------------------------------------------------------------- power priming
+ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters, uint64_t init_seed, float* W,
+                             double* theta_hist_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, m));
+  if (!W || iters < 0) return set_error(c, PPCA_ERR_INVALID_ARG, "null W or iters < 0");
+  const int64_t d = X->d;
+  if (init_seed) {
+    PPCA_TRY(init_rows(c, init_seed, W, m, d));
+    PPCA_TRY(cholqr2(c, W, m, d, 0.0, nullptr));
+  }
+  // all scratch up front (no reallocation while the side stream is busy)
+  float* Z = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
+  double* Sbuf = (double*)scratch(c, S_S, (size_t)4 * m * m * sizeof(double));      // S[2], Bm[2]
+  double* theta_dev = (double*)scratch(c, S_TC2, (size_t)std::max(1, iters) * m * sizeof(double) + (size_t)m * m * sizeof(double));
+  double* Rdummy = theta_dev + (size_t)std::max(1, iters) * m;
+  if (!Z || !Sbuf || !theta_dev) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  PassPlan plan;
+  PPCA_TRY(pass_prepare(c, X, m, &plan));
+  // pre-touch the scratch the loop uses so no allocation happens while the side stream is busy
+  if (!scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double)) || !scratch(c, S_GRAM, (size_t)m * m * sizeof(double)) ||
+      !scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64) ||
+      !scratch(c, S_W2, (size_t)m * d * sizeof(float)))
+    return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  cudaEvent_t ev_main[2], ev_side[2];
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&ev_main[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_side[i], cudaEventDisableTiming);
+    cudaEventRecord(ev_side[i], c->side);
+  }
+  ppca_status st = PPCA_OK;
+  for (int t = 0; t < iters && st == PPCA_OK; ++t) {
+    double* S = Sbuf + (size_t)(t & 1) * m * m;
+    double* Bm = Sbuf + (size_t)(2 + (t & 1)) * m * m;
+    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);
+    st = pass_power(c, X, &plan, W, m, Z, S);               // Z = YᵀX, S = YᵀY  (local)
+    if (st != PPCA_OK) break;
+    st = allreduce(c, Z, (size_t)m * d, false);
+    if (st == PPCA_OK) st = allreduce(c, S, (size_t)m * m, true);
+    if (st != PPCA_OK) break;
+    if (theta_hist_host) {
+      st = vec_gram(c, W, m, d, Bm);
+      if (st != PPCA_OK) break;
+      cudaEventRecord(ev_main[t & 1], c->stream);
+      cudaStreamWaitEvent(c->side, ev_main[t & 1], 0);
+      st = ritz_solve(c, S, Bm, m, theta_dev + (size_t)t * m, Rdummy, c->side);
+      cudaEventRecord(ev_side[t & 1], c->side);
+      if (st != PPCA_OK) break;
+    }
+    st = check_cuda(c, cudaMemcpyAsync(W, Z, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                    "copy Z");
+    if (st == PPCA_OK) st = cholqr2(c, W, m, d, 0.0, nullptr);
+  }
+  ppca_status st2 = finish(c, "ppca_prime_power");
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(ev_main[i]);
+    cudaEventDestroy(ev_side[i]);
+  }
+  if (st != PPCA_OK) return st;
+  if (st2 != PPCA_OK) return st2;
+  if (theta_hist_host && iters > 0) {
+    if (cudaMemcpy(theta_hist_host, theta_dev, (size_t)iters * m * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return set_error(c, PPCA_ERR_CUDA, "copy theta");
+  }
+  return PPCA_OK;
+}
+
+// ---------------------------------------------------------------------------- minibatch primings
+static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int batch, int64_t steps, uint64_t init_seed,
+                                    float* W, float* vel, int64_t* step_io, bool eigengame, double alpha, double mu) {
+  PPCA_TRY(check_matrix(c, X, m));
+  if (!W || !vel || !step_io || steps < 0 || batch < 1) return set_error(c, PPCA_ERR_INVALID_ARG, "bad minibatch args");
+  if (batch % c->world) return set_error(c, PPCA_ERR_INVALID_ARG, "world must divide batch");
+  if (c->world > 1 && (X->layout != PPCA_LAYOUT_INTERLEAVED || X->block_rows != batch))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "minibatch priming on >1 GPU needs the INTERLEAVED layout with block_rows == batch");
+  if (((X->n_global % batch) % c->world) != 0) return set_error(c, PPCA_ERR_INVALID_ARG, "world must divide the last block");
+  const int64_t d = X->d;
+  if (init_seed) {
+    PPCA_TRY(init_rows(c, init_seed, W, m, d));
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(vel, 0, (size_t)m * d * sizeof(float), c->stream), "zero velocity"));
+  }
+  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, batch / c->world) * m * sizeof(float));
+  float* Q = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
+  double* P = (double*)scratch(c, S_S, (size_t)m * m * sizeof(double));
+  if (!Y || !Q || !P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  int64_t s0 = *step_io;
+  for (int64_t s = s0; s < s0 + steps; ++s) {
+    int64_t r0, rows;
+    block_range(X, c->world, batch, s, &r0, &rows);
+    PPCA_TRY(xw(c, X, r0, rows, W, m, Y));
+    PPCA_TRY(ytx(c, X, r0, rows, Y, m, Q));
+    PPCA_TRY(yty(c, Y, m, rows, P));
+    PPCA_TRY(allreduce(c, Q, (size_t)m * d, false));
+    PPCA_TRY(allreduce(c, P, (size_t)m * m, true));
+    if (eigengame)
+      PPCA_TRY(eigengame_update(c, Q, P, W, vel, m, d, alpha, mu));
+    else
+      PPCA_TRY(oja_update(c, Q, P, W, vel, m, d, alpha, mu));
+  }
+  *step_io = s0 + steps;
+  return PPCA_OK;
+}
+
+ppca_status ppca_prime_oja(ppca_ctx* h, const ppca_matrix* X, int m, int batch, double alpha, double momentum,
+                           int64_t steps, uint64_t init_seed, float* W, float* velocity, int64_t* step_io) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(minibatch_common(c, X, m, batch, steps, init_seed, W, velocity, step_io, false, alpha, momentum));
+  return finish(c, "ppca_prime_oja");
+}
+
+ppca_status ppca_prime_eigengame(ppca_ctx* h, const ppca_matrix* X, int m, int batch, double alpha, double momentum,
+                                 int64_t steps, uint64_t init_seed, float* V, float* velocity, int64_t* step_io) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(minibatch_common(c, X, m, batch, steps, init_seed, V, velocity, step_io, true, alpha, momentum));
+  return finish(c, "ppca_prime_eigengame");
+}
+
+// ---------------------------------------------------------------------------- refine
+ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, float* E, double* theta_host,
+                        int* subspace_dim) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, m));
+  if (!V || !E || k < 1 || k > m) return set_error(c, PPCA_ERR_INVALID_ARG, "bad refine args (k=%d, m=%d)", k, m);
+  const int64_t d = X->d;
+  float* B = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
+  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
+  double* S = (double*)scratch(c, S_S, (size_t)2 * m * m * sizeof(double));
+  double* out = (double*)scratch(c, S_TC2, (size_t)m * sizeof(double) + (size_t)m * m * sizeof(double));
+  if (!B || !Y || !S || !out) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  double* Bm = S + (size_t)m * m;
+  double* theta_dev = out;
+  double* R = out + m;
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream), "copy V"));
+  PPCA_TRY(normalize_rows(c, B, m, d));                 // current_components
+  int mm = m;
+  // B = orth(V); a direction whose relative residual is < 1e-6 is dropped (SPEC L51 drops < 1e-10 in
+  // fp64; fp32 inputs cannot resolve residuals below ~1e-7 — DESIGN.md reading R14)
+  PPCA_TRY(cholqr2(c, B, m, d, 1e-6, &mm));
+  if (mm < k) {
+    finish(c, "ppca_refine");
+    return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "only %d of %d directions survive", mm, k);
+  }
+  PassPlan plan;
+  PPCA_TRY(pass_prepare(c, X, mm, &plan));
+  PPCA_TRY(pass_gram(c, X, &plan, B, mm, S));            // S = (XBᵀ)ᵀ(XBᵀ)
+  PPCA_TRY(allreduce(c, S, (size_t)mm * mm, true));
+  PPCA_TRY(vec_gram(c, B, mm, d, Bm));
+  PPCA_TRY(ritz_solve(c, S, Bm, mm, theta_dev, R, c->stream));
+  PPCA_TRY(lift_rows(c, R, mm, B, mm, k, d, E, true, c->stream));
+  PPCA_TRY(finish(c, "ppca_refine"));
+  if (theta_host && cudaMemcpy(theta_host, theta_dev, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy theta");
+  if (subspace_dim) *subspace_dim = mm;
+  return PPCA_OK;
+}
+
+// ---------------------------------------------------------------------------- eval / support
+ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_t d, const double* thr_host, int nthr,
+                      double* angles_host, int* lces_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  if (!E || !T || k < 1 || d < 1 || (nthr > 0 && (!thr_host || !lces_host)))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "bad eval args");
+  double* dots = (double*)scratch(c, S_ROWRED, (size_t)std::max(k, PPCA_MAX_M) * sizeof(double));
+  PPCA_TRY(row_dots(c, E, T, k, d, dots));
+  PPCA_TRY(finish(c, "ppca_eval"));
+  std::vector<double> hd(k), ang(k);
+  if (cudaMemcpy(hd.data(), dots, k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy dots");
+  for (int i = 0; i < k; ++i) ang[i] = acos(std::min(1.0, fabs(hd[i])));
+  if (angles_host) memcpy(angles_host, ang.data(), k * sizeof(double));
+  for (int t = 0; t < nthr; ++t) {
+    int s = 0;
+    while (s < k && ang[s] < thr_host[t]) ++s;
+    lces_host[t] = s;
+  }
+  return PPCA_OK;
+}
+
+ppca_status ppca_captured_variance(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, double* var_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, m));
+  if (!V || !var_host) return set_error(c, PPCA_ERR_INVALID_ARG, "null V / output");
+  double* S = (double*)scratch(c, S_S, (size_t)m * m * sizeof(double));
+  PassPlan plan;
+  PPCA_TRY(pass_prepare(c, X, m, &plan));
+  PPCA_TRY(pass_gram(c, X, &plan, V, m, S));
+  PPCA_TRY(allreduce(c, S, (size_t)m * m, true));
+  PPCA_TRY(finish(c, "ppca_captured_variance"));
+  std::vector<double> hs((size_t)m * m);
+  if (cudaMemcpy(hs.data(), S, hs.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy S");
+  for (int i = 0; i < m; ++i) var_host[i] = hs[(size_t)i * m + i];
+  return PPCA_OK;
+}
+
+ppca_status ppca_gram(ppca_ctx* h, const ppca_matrix* X, double* G) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, 1));
+  if (!G) return set_error(c, PPCA_ERR_INVALID_ARG, "null G");
+  const int64_t d = X->d;
+  int ns = tn_pick_splits(c, d, d, X->n_local);
+  double* P = (double*)scratch(c, S_PART, (size_t)ns * d * d * sizeof(double));
+  if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed (d=%lld)", (long long)d);
+  if (X->dtype == PPCA_F32)
+    PPCA_TRY((launch_tn_splitk<float, float>(c, (const float*)X->data, X->ld, (const float*)X->data, X->ld, P, d, d,
+                                             X->n_local, ns)));
+  else
+    PPCA_TRY((launch_tn_splitk<__nv_bfloat16, __nv_bfloat16>(c, (const __nv_bfloat16*)X->data, X->ld,
+                                                             (const __nv_bfloat16*)X->data, X->ld, P, d, d,
+                                                             X->n_local, ns)));
+  PPCA_TRY(launch_reduce_splits_f64(c, P, ns, d * d, G));
+  PPCA_TRY(allreduce(c, G, (size_t)d * d, true));
+  return finish(c, "ppca_gram");
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// common.cuh — shared internals of libppca (context, errors, scratch, Philox, small helpers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/ppca.h"
+
+namespace ppca {
+
+// ----------------------------------------------------------------------------- device error word
+// Kernels set bits here instead of trapping; the host reads it once per ABI call.
+enum DevErr : int {
+  DEV_OK = 0,
+  DEV_NONFINITE = 1,
+  DEV_DEGENERATE = 2,
+  DEV_COLLAPSE = 4,
+  DEV_NOCONV = 8,
+};
+
+struct Ctx;
+typedef ppca_status (*AllreduceFn)(Ctx*, void* buf, size_t count, int is_f64);
+
+struct Ctx {
+  int device = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // side stream (Ritz solves overlap the next pass)
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  void* nccl_comm = nullptr;          // ncclComm_t when world > 1
+  int* d_err = nullptr;               // device error word
+  int pass_impl = 0;                  // 0 auto, 1 simt, 2 tcgen05
+  int last_impl = 0;                  // implementation of the most recent pass
+  int sm_count = 148;
+  int64_t launches = 0;
+  // pass timing (bench): event pairs recorded around each pass
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;
+  size_t tev_used = 0;
+  std::string last_error;
+  // grow-only scratch slots
+  static const int kSlots = 24;
+  void* slot_ptr[kSlots] = {};
+  size_t slot_bytes[kSlots] = {};
+};
+
+// scratch slot ids
+enum Slot {
+  S_PART = 0,    // split-K partials (fp64/fp32)
+  S_Y,           // Y = X·Wᵀ (n_local × m)
+  S_Z,           // Z (m × d) fp32
+  S_S,           // S (m × m) fp64 (+ allreduce payload)
+  S_GRAM,        // m×m fp64 gram of vectors
+  S_SMALL,       // small fp64 work (L, Linv, U, R ...)
+  S_W2,          // m × d fp32 temp
+  S_W3,          // m × d fp32 temp
+  S_ROWRED,      // per-row reductions
+  S_GEN0, S_GEN1, S_GEN2, S_GEN3,  // generator buffers
+  S_EVAL,
+  S_TC0, S_TC1, S_TC2,             // tensor-core pass scratch
+  S_NTSTAGE,
+};
+
+void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory
+
+ppca_status set_error(Ctx* c, ppca_status s, const char* fmt, ...);
+ppca_status check_cuda(Ctx* c, cudaError_t e, const char* what);
+ppca_status finish(Ctx* c, const char* what);      // sync stream, read error word, map to status
+ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64);
+
+#define PPCA_TRY(expr)                         \
+  do {                                         \
+    ppca_status _s = (expr);                   \
+    if (_s != PPCA_OK) return _s;              \
+  } while (0)
+
+#define PPCA_LAUNCH_CHECK(c, what)                                        \
+  do {                                                                    \
+    (c)->launches++;                                                      \
+    cudaError_t _e = cudaGetLastError();                                  \
+    if (_e != cudaSuccess) return check_cuda((c), _e, what);              \
+  } while (0)
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline size_t elt_size(ppca_dtype t) { return t == PPCA_BF16 ? 2 : 4; }
+
+// ----------------------------------------------------------------------------- element loads
+__device__ __forceinline__ float load_elt(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float load_elt(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+
+// ----------------------------------------------------------------------------- Philox4x32-10
+// Salmon et al. (SC'11); identical to curand_Philox4x32_10.  Counter convention:
+// ctr = (call_lo, call_hi, stream, 0), key = (seed_lo, seed_hi); element e uses word e % 4 of call e / 4.
+__host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+}
+
+__host__ __device__ __forceinline__ uint32_t philox_word(uint64_t seed, uint32_t stream, uint64_t e) {
+  uint64_t call = e >> 2;
+  uint32_t c[4] = {(uint32_t)call, (uint32_t)(call >> 32), stream, 0u};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  return c[e & 3];
+}
+
+__host__ __device__ __forceinline__ double u32_to_unit(uint32_t w) { return ((double)w + 0.5) * 2.3283064365386963e-10; }
+
+// Gaussian element e of a stream: Box–Muller on the word pair (2⌊e/2⌋, 2⌊e/2⌋+1).
+__device__ __forceinline__ double gaussian_elt(uint64_t seed, uint32_t stream, uint64_t e) {
+  uint64_t pair = e >> 1;
+  uint64_t call = pair >> 1;
+  uint32_t c[4] = {(uint32_t)call, (uint32_t)(call >> 32), stream, 0u};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t w0 = (pair & 1) ? c[2] : c[0];
+  uint32_t w1 = (pair & 1) ? c[3] : c[1];
+  double u0 = u32_to_unit(w0), u1 = u32_to_unit(w1);
+  double rad = sqrt(-2.0 * log(u0));
+  double ang = 6.283185307179586 * u1;
+  return (e & 1) ? rad * sin(ang) : rad * cos(ang);
+}
+
+__device__ __forceinline__ double exponential_elt(uint64_t seed, uint32_t stream, uint64_t e) {
+  return -log(u32_to_unit(philox_word(seed, stream, e)));
+}
+
+// RNE fp64 → bf16 (bit trick on the fp64 significand; exact for the normal range).
+__device__ __forceinline__ __nv_bfloat16 f64_to_bf16_rne(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  unsigned long long lsb = (b >> 45) & 1ull;
+  b = (b + ((1ull << 44) - 1ull) + lsb) & ~((1ull << 45) - 1ull);
+  float f = (float)__longlong_as_double((long long)b);   // exact: 8 significant bits
+  unsigned int u = __float_as_uint(f) >> 16;
+  __nv_bfloat16_raw r;
+  r.x = (unsigned short)u;
+  return __nv_bfloat16(r);
+}
+
+// ----------------------------------------------------------------------------- reductions
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace ppca

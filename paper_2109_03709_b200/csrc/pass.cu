@@ -1,0 +1,137 @@
+// pass.cu — SIMT implementation of the streaming pass (impl 1) and the dispatcher.
+#include "pass.cuh"
+#include "gemm_simt.cuh"
+
+namespace ppca {
+
+// Y = X·Wᵀ for local rows [r0, r0+rows)
+ppca_status xw(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* W, int m, float* Y) {
+  if (X->dtype == PPCA_F32)
+    return launch_nt<float>(c, (const float*)X->data + r0 * X->ld, X->ld, W, X->d, Y, m, rows, m, X->d);
+  return launch_nt<__nv_bfloat16>(c, (const __nv_bfloat16*)X->data + r0 * X->ld, X->ld, W, X->d, Y, m, rows, m, X->d);
+}
+
+// Z (fp32 m×d) = Yᵀ X[r0:r0+rows]
+ppca_status ytx(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* Y, int m, float* Z) {
+  int ns = tn_pick_splits(c, m, X->d, rows);
+  double* P = (double*)scratch(c, S_PART, (size_t)ns * m * X->d * sizeof(double));
+  if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (X->dtype == PPCA_F32)
+    PPCA_TRY((launch_tn_splitk<float, float>(c, Y, m, (const float*)X->data + r0 * X->ld, X->ld, P, m, X->d, rows, ns)));
+  else
+    PPCA_TRY((launch_tn_splitk<float, __nv_bfloat16>(c, Y, m, (const __nv_bfloat16*)X->data + r0 * X->ld, X->ld, P, m,
+                                                    X->d, rows, ns)));
+  return launch_reduce_splits_f32(c, P, ns, (int64_t)m * X->d, Z, X->d, X->d);
+}
+
+// S (fp64 m×m) = YᵀY
+ppca_status yty(Ctx* c, const float* Y, int m, int64_t rows, double* S) {
+  int ns = tn_pick_splits(c, m, m, rows);
+  double* P = (double*)scratch(c, S_NTSTAGE, (size_t)ns * m * m * sizeof(double));
+  if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  PPCA_TRY((launch_tn_splitk<float, float>(c, Y, m, Y, m, P, m, m, rows, ns)));
+  return launch_reduce_splits_f64(c, P, ns, (int64_t)m * m, S);
+}
+
+
+ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan);
+ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S);
+ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S);
+void pass_tc_release(Ctx* c);
+
+ppca_status pass_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan) {
+  plan->impl = 1;
+  if (c->pass_impl == 1) return PPCA_OK;
+  ppca_status s = pass_tc_prepare(c, X, m, plan);
+  if (s == PPCA_OK) return PPCA_OK;
+  if (c->pass_impl == 2) return s;         // explicitly requested: report why it cannot run
+  plan->impl = 1;                          // auto: shapes the tensor-core pass does not cover
+  return PPCA_OK;
+}
+
+static cudaEvent_t timing_event(Ctx* c) {
+  if (c->tev_used == c->tev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->tev.push_back(e);
+  }
+  return c->tev[c->tev_used++];
+}
+
+struct PassTimer {
+  Ctx* c;
+  explicit PassTimer(Ctx* cc) : c(cc) {
+    if (c->timing) cudaEventRecord(timing_event(c), c->stream);
+  }
+  ~PassTimer() {
+    if (c->timing) cudaEventRecord(timing_event(c), c->stream);
+  }
+};
+
+static ppca_status pass_power_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
+                                   float* Z, double* S);
+static ppca_status pass_gram_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
+                                  double* S);
+
+ppca_status pass_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S) {
+  PassTimer t(c);
+  c->last_impl = plan->impl;
+  return pass_power_impl(c, X, plan, W, m, Z, S);
+}
+
+ppca_status pass_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S) {
+  PassTimer t(c);
+  c->last_impl = plan->impl;
+  return pass_gram_impl(c, X, plan, W, m, S);
+}
+
+ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n) {
+  cudaStreamSynchronize(c->stream);
+  double tot = 0.0;
+  int64_t cnt = 0;
+  for (size_t i = 0; i + 1 < c->tev_used; i += 2) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->tev[i], c->tev[i + 1]) == cudaSuccess) {
+      tot += t;
+      ++cnt;
+    }
+  }
+  cudaGetLastError();
+  c->tev_used = 0;
+  *ms = tot;
+  *n = cnt;
+  return PPCA_OK;
+}
+
+static ppca_status pass_power_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
+                                   float* Z, double* S) {
+  if (plan->impl == 2) return pass_tc_power(c, X, plan, W, m, Z, S);
+  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
+  if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (X->n_local == 0) {
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(Z, 0, (size_t)m * X->d * sizeof(float), c->stream), "memset"));
+    return check_cuda(c, cudaMemsetAsync(S, 0, (size_t)m * m * sizeof(double), c->stream), "memset");
+  }
+  PPCA_TRY(xw(c, X, 0, X->n_local, W, m, Y));
+  PPCA_TRY(ytx(c, X, 0, X->n_local, Y, m, Z));
+  return yty(c, Y, m, X->n_local, S);
+}
+
+static ppca_status pass_gram_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
+                                  double* S) {
+  if (plan->impl == 2) return pass_tc_gram(c, X, plan, W, m, S);
+  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
+  if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (X->n_local == 0) return check_cuda(c, cudaMemsetAsync(S, 0, (size_t)m * m * sizeof(double), c->stream), "memset");
+  PPCA_TRY(xw(c, X, 0, X->n_local, W, m, Y));
+  return yty(c, Y, m, X->n_local, S);
+}
+
+void pass_release(Ctx* c) {
+  pass_tc_release(c);
+  for (auto e : c->tev) cudaEventDestroy(e);
+  c->tev.clear();
+  c->tev_used = 0;
+}
+
+}  // namespace ppca

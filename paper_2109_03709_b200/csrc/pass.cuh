@@ -1,0 +1,26 @@
+// pass.cuh — the streaming pass over X (§8 rows a2 / a7): one interface, two implementations.
+//   impl 1 (SIMT):    Y = X·Wᵀ (CUDA-core tiles), then Z = YᵀX and S = YᵀY (split-K, fp32→fp64).
+//   impl 2 (tcgen05): fused tensor-core pass (pass_tc.cu) — X staged once per tile.
+#pragma once
+#include "common.cuh"
+
+namespace ppca {
+
+struct PassPlan {
+  int impl = 1;
+};
+
+ppca_status pass_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan);
+// power mode: Z[m][d] (fp32) = (X·Wᵀ)ᵀX over the local rows, S[m][m] (fp64) = (X·Wᵀ)ᵀ(X·Wᵀ)
+ppca_status pass_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S);
+// refine mode: S only
+ppca_status pass_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S);
+void pass_release(Ctx* c);
+ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n);
+
+// building blocks (SIMT), local rows [r0, r0+rows)
+ppca_status xw(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* W, int m, float* Y);
+ppca_status ytx(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* Y, int m, float* Z);
+ppca_status yty(Ctx* c, const float* Y, int m, int64_t rows, double* S);
+
+}  // namespace ppca

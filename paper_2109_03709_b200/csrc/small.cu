@@ -1,0 +1,587 @@
+// small.cu — m×m side of the hot path (see small.cuh).  All m×m arithmetic is fp64.
+#include "small.cuh"
+#include "gemm_simt.cuh"
+
+namespace ppca {
+
+// ============================================================================ vector Gram
+// G_ij = Σ_x V[i][x] V[j][x]; tile 32×32 outputs × 64-column chunks, split over d.
+__global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__ V, int m, int64_t d,
+                                                       int64_t cols_per_split, double* __restrict__ P) {
+  __shared__ float Vi[32][65];
+  __shared__ float Vj[32][65];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int64_t xb = (int64_t)blockIdx.z * cols_per_split;
+  const int64_t xe = min(d, xb + cols_per_split);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // ty 0..7 → rows ty*4..+4
+  double acc[4] = {0, 0, 0, 0};
+  for (int64_t x0 = xb; x0 < xe; x0 += 64) {
+    for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+      int r = e / 64, cidx = e % 64;
+      int64_t x = x0 + cidx;
+      Vi[r][cidx] = (i0 + r < m && x < xe) ? V[(int64_t)(i0 + r) * d + x] : 0.f;
+      Vj[r][cidx] = (j0 + r < m && x < xe) ? V[(int64_t)(j0 + r) * d + x] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int cidx = 0; cidx < 64; ++cidx) {
+      double b = (double)Vj[tx][cidx];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[a] = fma((double)Vi[ty * 4 + a][cidx], b, acc[a]);
+    }
+    __syncthreads();
+  }
+  double* Pz = P + (int64_t)blockIdx.z * m * m;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    int i = i0 + ty * 4 + a, j = j0 + tx;
+    if (i < m && j < m) Pz[(int64_t)i * m + j] = acc[a];
+  }
+}
+
+ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G) {
+  int tiles = (int)ceil_div(m, 32);
+  int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
+  int64_t maxs = ceil_div(d, 256);
+  int nsplit = (int)std::max<int64_t>(1, std::min(want, maxs));
+  int64_t cps = ceil_div(ceil_div(d, nsplit), 64) * 64;
+  nsplit = (int)ceil_div(d, cps);
+  double* P = (double*)scratch(c, S_PART, (size_t)nsplit * m * m * sizeof(double));
+  if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  vec_gram_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, c->stream>>>(V, m, d, cps, P);
+  PPCA_LAUNCH_CHECK(c, "vec_gram");
+  return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G);
+}
+
+// ============================================================================ Cholesky (one CTA)
+// In smem A[m][m] (fp64).  Right-looking; pivots ≤ drop²·G_jj are dropped (column zeroed) if
+// drop > 0, else flag COLLAPSE.  Writes Linv (lower, dropped rows zero) and keep[] flags.
+__device__ void block_cholesky(double* A, int m, double drop, int* keep, double* diag0, int* d_err) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < m; i += nt) diag0[i] = A[i * m + i];
+  __syncthreads();
+  __shared__ double piv;
+  __shared__ int dropped;
+  for (int j = 0; j < m; ++j) {
+    if (tid == 0) {
+      double p = A[j * m + j];
+      int dr = 0;
+      if (drop > 0.0) {
+        dr = !(p > drop * drop * diag0[j]);
+      } else if (!(p > 0.0) || !isfinite(p)) {
+        atomicOr(d_err, DEV_COLLAPSE);
+        dr = 1;
+      }
+      dropped = dr;
+      keep[j] = !dr;
+      piv = dr ? 0.0 : sqrt(p);
+    }
+    __syncthreads();
+    if (dropped) {
+      for (int i = j + tid; i < m; i += nt) A[i * m + j] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    for (int i = j + tid; i < m; i += nt) A[i * m + j] = (i == j) ? piv : A[i * m + j] / piv;
+    __syncthreads();
+    const int rem = m - j - 1;
+    for (int e = tid; e < rem * rem; e += nt) {
+      int i = j + 1 + e / rem, k = j + 1 + e % rem;
+      if (k <= i) A[i * m + k] -= A[i * m + j] * A[k * m + j];
+    }
+    __syncthreads();
+  }
+}
+
+// Forward substitution: Linv (global, row-major m×m), thread per column.
+__device__ void block_lower_inverse(const double* L, int m, const int* keep, double* Linv) {
+  for (int cc = threadIdx.x; cc < m; cc += blockDim.x) {
+    for (int i = 0; i < m; ++i) {
+      double v = 0.0;
+      if (i >= cc && keep[i]) {
+        double s = (i == cc) ? 1.0 : 0.0;
+        for (int j = cc; j < i; ++j) s -= L[i * m + j] * Linv[(int64_t)j * m + cc];
+        v = s / L[i * m + i];
+      }
+      Linv[(int64_t)i * m + cc] = v;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop, double* __restrict__ Linv,
+                                int* __restrict__ row_map, int* __restrict__ m_out, int* d_err) {
+  extern __shared__ double sm[];
+  double* A = sm;                                  // m*m
+  double* diag0 = A + m * m;                       // m
+  int* keep = (int*)(diag0 + m);                   // m
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) A[e] = G[e];
+  __syncthreads();
+  block_cholesky(A, m, drop, keep, diag0, d_err);
+  block_lower_inverse(A, m, keep, Linv);
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int i = 0; i < m; ++i) row_map[i] = keep[i] ? o++ : -1;
+    *m_out = o;
+  }
+}
+
+// ============================================================================ apply: OUT = C · IN
+// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower).  Block: 8 warps × 32 lanes,
+// 128 columns (4 per lane); C staged in smem as fp64.
+__global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
+                                                         int m_in, const int* __restrict__ row_map,
+                                                         bool lower, const float* __restrict__ IN,
+                                                         int64_t d, float* __restrict__ OUT) {
+  extern __shared__ double cs[];                 // rows * m_in
+  for (int e = threadIdx.x; e < rows * m_in; e += blockDim.x) cs[e] = C[(int64_t)(e / m_in) * ldc + e % m_in];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t x0 = (int64_t)blockIdx.x * 128 + lane;
+  for (int i = warp; i < rows; i += 8) {
+    int oi = row_map ? row_map[i] : i;
+    if (oi < 0) continue;
+    double acc[4] = {0, 0, 0, 0};
+    int jend = lower ? i + 1 : m_in;
+    for (int j = 0; j < jend; ++j) {
+      double cij = cs[i * m_in + j];
+      if (cij == 0.0) continue;
+      const float* in = IN + (int64_t)j * d;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int64_t x = x0 + q * 32;
+        if (x < d) acc[q] = fma(cij, (double)in[x], acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int64_t x = x0 + q * 32;
+      if (x < d) OUT[(int64_t)oi * d + x] = (float)acc[q];
+    }
+  }
+}
+
+static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
+                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
+  size_t smem = (size_t)rows * m_in * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  apply_rows_kernel<<<(unsigned)ceil_div(d, 128), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN,
+                                                                  d, OUT);
+  PPCA_LAUNCH_CHECK(c, "apply_rows");
+  return PPCA_OK;
+}
+
+// ============================================================================ CholQR2
+ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out) {
+  double* G = (double*)scratch(c, S_GRAM, (size_t)m * m * sizeof(double));
+  double* Linv = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64);
+  int* row_map = (int*)(Linv + (size_t)m * m);
+  int* d_mout = row_map + m;
+  float* T = (float*)scratch(c, S_W2, (size_t)m * d * sizeof(float));
+  if (!G || !Linv || !T) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + m * sizeof(int);
+  for (int pass = 0; pass < 2; ++pass) {
+    PPCA_TRY(vec_gram(c, W, m, d, G));
+    chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, pass == 0 ? drop_tol : 0.0, Linv, row_map, d_mout,
+                                                 c->d_err);
+    PPCA_LAUNCH_CHECK(c, "chol_inv");
+    if (pass == 0 && drop_tol > 0.0) {
+      int h_m = m;
+      PPCA_TRY(check_cuda(c, cudaMemcpyAsync(&h_m, d_mout, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+                          "copy m_out"));
+      PPCA_TRY(check_cuda(c, cudaStreamSynchronize(c->stream), "sync m_out"));
+      PPCA_TRY(apply_rows(c, Linv, m, m, m, row_map, true, W, d, T, c->stream));
+      PPCA_TRY(check_cuda(c, cudaMemcpyAsync(W, T, (size_t)h_m * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                                             c->stream), "copy W"));
+      m = h_m;
+      if (m_out) *m_out = h_m;
+      if (m == 0) return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "all vectors collapsed");
+      continue;
+    }
+    PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, W, d, T, c->stream));
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(W, T, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                                           c->stream), "copy W"));
+  }
+  if (m_out && drop_tol <= 0.0) *m_out = m;
+  return PPCA_OK;
+}
+
+// ============================================================================ Rayleigh–Ritz (one CTA)
+__device__ __forceinline__ void jacobi_pair(int r, int i, int mm, int& p, int& q) {
+  // circle method: player 0 fixed, players 1..mm-1 rotate; position j holds ((j + r) % (mm-1)) + 1
+  int a, b;
+  if (i == 0) {
+    a = 0;
+    b = (r % (mm - 1)) + 1;
+  } else {
+    a = ((i + r) % (mm - 1)) + 1;
+    b = ((mm - 1 - i + r) % (mm - 1)) + 1;
+  }
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+// smem: A[m*m] (fp64) + small arrays.  Global scratch: Linv[m*m], Vg[m*m], T1[m*m].
+__global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
+                                                   int m, double* __restrict__ Linv, double* __restrict__ Vg,
+                                                   double* __restrict__ T1, double* __restrict__ theta,
+                                                   double* __restrict__ R, int* d_err) {
+  extern __shared__ double sm[];
+  double* A = sm;                       // m*m
+  double* diag0 = A + m * m;            // m
+  double* csn = diag0 + m;              // 2 * 64 (c, s) for up to 64 pairs
+  int* keep = (int*)(csn + 2 * (PPCA_MAX_M / 2 + 1));
+  int* pq = keep + m;                   // 2 * pairs
+  int* perm = pq + 2 * (PPCA_MAX_M / 2 + 1);
+  __shared__ double red[2][32];
+  __shared__ int converged;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // 1. L = chol(Bm), Linv
+  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
+  __syncthreads();
+  block_cholesky(A, m, 0.0, keep, diag0, d_err);
+  block_lower_inverse(A, m, keep, Linv);
+  // 2. C = Linv · S · Linvᵀ :  T1 = S · Linvᵀ  then  A = Linv · T1
+  for (int e = tid; e < m * m; e += nt) {
+    int i = e / m, j = e % m;
+    double s = 0.0;
+    for (int t = 0; t <= j; ++t) s += S[i * m + t] * Linv[(int64_t)j * m + t];
+    T1[e] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) {
+    int i = e / m, j = e % m;
+    double s = 0.0;
+    for (int t = 0; t <= i; ++t) s += Linv[(int64_t)i * m + t] * T1[t * m + j];
+    A[e] = s;
+  }
+  __syncthreads();
+  // symmetrise
+  for (int e = tid; e < m * m; e += nt) {
+    int i = e / m, j = e % m;
+    if (i < j) {
+      double v = 0.5 * (A[i * m + j] + A[j * m + i]);
+      A[i * m + j] = v;
+      A[j * m + i] = v;
+    }
+  }
+  for (int e = tid; e < m * m; e += nt) Vg[e] = (e / m == e % m) ? 1.0 : 0.0;
+  __syncthreads();
+  // 3. parallel cyclic Jacobi (circle ordering), ≤ 100 sweeps, off < 1e-12·‖diag‖
+  const int mm = (m + 1) & ~1;
+  const int npairs = mm / 2;
+  for (int sweep = 0; sweep <= 100; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      double v = A[e];
+      if (e / m == e % m) dg += v * v; else off += v * v;
+    }
+    off = warp_sum(off);
+    dg = warp_sum(dg);
+    if ((tid & 31) == 0) { red[0][tid >> 5] = off; red[1][tid >> 5] = dg; }
+    __syncthreads();
+    if (tid == 0) {
+      double o = 0, g = 0;
+      for (int w = 0; w < nt / 32; ++w) { o += red[0][w]; g += red[1][w]; }
+      converged = (sqrt(o) <= 1e-12 * sqrt(g)) || o == 0.0;
+      if (!converged && sweep == 100) atomicOr(d_err, DEV_NOCONV);
+    }
+    __syncthreads();
+    if (converged || sweep == 100) break;
+    for (int r = 0; r < mm - 1; ++r) {
+      for (int i = tid; i < npairs; i += nt) {
+        int p, q;
+        jacobi_pair(r, i, mm, p, q);
+        double cc = 1.0, ss = 0.0;
+        if (q < m) {
+          double apq = A[p * m + q];
+          if (apq != 0.0) {
+            double tau = (A[q * m + q] - A[p * m + p]) / (2.0 * apq);
+            double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            cc = 1.0 / sqrt(1.0 + t * t);
+            ss = t * cc;
+          }
+        }
+        pq[2 * i] = p;
+        pq[2 * i + 1] = q;
+        csn[2 * i] = cc;
+        csn[2 * i + 1] = ss;
+      }
+      __syncthreads();
+      // columns of A and V:  (x_p, x_q) ← (c x_p − s x_q, s x_p + c x_q)
+      for (int e = tid; e < npairs * m; e += nt) {
+        int i = e / m, row = e % m;
+        int p = pq[2 * i], q = pq[2 * i + 1];
+        double cc = csn[2 * i], ss = csn[2 * i + 1];
+        if (q >= m || ss == 0.0) continue;
+        double ap = A[row * m + p], aq = A[row * m + q];
+        A[row * m + p] = cc * ap - ss * aq;
+        A[row * m + q] = ss * ap + cc * aq;
+        double vp = Vg[row * m + p], vq = Vg[row * m + q];
+        Vg[row * m + p] = cc * vp - ss * vq;
+        Vg[row * m + q] = ss * vp + cc * vq;
+      }
+      __syncthreads();
+      // rows of A
+      for (int e = tid; e < npairs * m; e += nt) {
+        int i = e / m, col = e % m;
+        int p = pq[2 * i], q = pq[2 * i + 1];
+        double cc = csn[2 * i], ss = csn[2 * i + 1];
+        if (q >= m || ss == 0.0) continue;
+        double ap = A[p * m + col], aq = A[q * m + col];
+        A[p * m + col] = cc * ap - ss * aq;
+        A[q * m + col] = ss * ap + cc * aq;
+      }
+      __syncthreads();
+    }
+  }
+  // 4. sort descending (ties by index) and R = U_sortedᵀ · Linv
+  for (int i = tid; i < m; i += nt) {
+    double li = A[i * m + i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      double lj = A[j * m + j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += nt) theta[i] = A[perm[i] * m + perm[i]];
+  for (int e = tid; e < m * m; e += nt) {
+    int i = e / m, j = e % m;          // R[i][j] = Σ_t V[t][perm i] Linv[t][j]
+    int col = perm[i];
+    double s = 0.0;
+    for (int t = j; t < m; ++t) s += Vg[t * m + col] * Linv[(int64_t)t * m + j];
+    R[e] = s;
+  }
+}
+
+ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev, double* R_dev,
+                       cudaStream_t stream) {
+  double* scr = (double*)scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double));
+  if (!scr) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + 2 * (PPCA_MAX_M / 2 + 1) * sizeof(double) +
+                (size_t)m * sizeof(int) + 2 * (PPCA_MAX_M / 2 + 1) * sizeof(int) + PPCA_MAX_M * sizeof(int);
+  ritz_kernel<<<1, 512, smem, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, scr + (size_t)2 * m * m, theta_dev,
+                                        R_dev, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "ritz_kernel");
+  return PPCA_OK;
+}
+
+// ============================================================================ sign convention, lift
+__global__ void sign_rows_kernel(float* __restrict__ E, int64_t d) {
+  float* row = E + (int64_t)blockIdx.x * d;
+  float best = -1.f;
+  int64_t bi = 0;
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
+    float a = fabsf(row[x]);
+    if (a > best) { best = a; bi = x; }        // first max within the thread's stride
+  }
+  __shared__ float sb[32];
+  __shared__ long long si[32];
+  // warp argmax (ties → lower index)
+  for (int o = 16; o > 0; o >>= 1) {
+    float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    long long oi = __shfl_xor_sync(0xffffffffu, (long long)bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  __shared__ float sgn;
+  if (threadIdx.x == 0) {
+    float b = sb[0];
+    long long i = si[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sb[w] > b || (sb[w] == b && si[w] < i)) { b = sb[w]; i = si[w]; }
+    sgn = row[i] < 0.f ? -1.f : 1.f;
+  }
+  __syncthreads();
+  if (sgn < 0.f)
+    for (int64_t x = threadIdx.x; x < d; x += blockDim.x) row[x] = -row[x];
+}
+
+ppca_status lift_rows(Ctx* c, const double* R, int ldr, const float* W, int m, int k, int64_t d, float* E,
+                      bool apply_sign, cudaStream_t stream) {
+  PPCA_TRY(apply_rows(c, R, ldr, k, m, nullptr, false, W, d, E, stream));
+  if (apply_sign) {
+    sign_rows_kernel<<<k, 256, 0, stream>>>(E, d);
+    PPCA_LAUNCH_CHECK(c, "sign_rows");
+  }
+  return PPCA_OK;
+}
+
+// ============================================================================ init / normalise
+__global__ void init_rows_kernel(uint64_t seed, float* __restrict__ W, int m, int64_t d) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)m * d) return;
+  W[e] = (float)gaussian_elt(seed, 6u, (uint64_t)e);
+}
+
+__global__ void row_norm_kernel(const float* __restrict__ W, int64_t d, double* __restrict__ nrm) {
+  const float* row = W + (int64_t)blockIdx.x * d;
+  double s = 0.0;
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) s += (double)row[x] * row[x];
+  s = warp_sum(s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    nrm[blockIdx.x] = sqrt(t);
+  }
+}
+
+__global__ void scale_rows_kernel(float* __restrict__ W, int m, int64_t d, const double* __restrict__ nrm,
+                                  int* d_err) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)m * d) return;
+  double n = nrm[e / d];
+  if (!(n > 1e-300)) {
+    atomicOr(d_err, DEV_DEGENERATE);
+    return;
+  }
+  double v = (double)W[e] / n;
+  if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
+  W[e] = (float)v;
+}
+
+ppca_status normalize_rows(Ctx* c, float* W, int m, int64_t d) {
+  double* nrm = (double*)scratch(c, S_ROWRED, (size_t)PPCA_MAX_M * sizeof(double));
+  row_norm_kernel<<<m, 256, 0, c->stream>>>(W, d, nrm);
+  PPCA_LAUNCH_CHECK(c, "row_norm");
+  scale_rows_kernel<<<(unsigned)ceil_div((int64_t)m * d, 256), 256, 0, c->stream>>>(W, m, d, nrm, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "scale_rows");
+  return PPCA_OK;
+}
+
+ppca_status init_rows(Ctx* c, uint64_t seed, float* W, int m, int64_t d) {
+  init_rows_kernel<<<(unsigned)ceil_div((int64_t)m * d, 256), 256, 0, c->stream>>>(seed, W, m, d);
+  PPCA_LAUNCH_CHECK(c, "init_rows");
+  return normalize_rows(c, W, m, d);
+}
+
+// ============================================================================ priming updates
+// Oja:  T = tril(P)·W  (apply), then elementwise  G = Q − T,  v ← μv + G,  W ← W + α(G + μv).
+__global__ void oja_elementwise_kernel(const float* __restrict__ Q, const float* __restrict__ T,
+                                       float* __restrict__ W, float* __restrict__ vel, int64_t count,
+                                       double alpha, double mu, int* d_err) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double g = (double)Q[e] - (double)T[e];
+  double v = mu * (double)vel[e] + g;
+  double w = (double)W[e] + alpha * (g + mu * v);
+  if (!isfinite(w)) atomicOr(d_err, DEV_NONFINITE);
+  vel[e] = (float)v;
+  W[e] = (float)w;
+}
+
+ppca_status oja_update(Ctx* c, const float* Q, const double* P, float* W, float* vel, int m, int64_t d,
+                       double alpha, double mu) {
+  float* T = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
+  PPCA_TRY(apply_rows(c, P, m, m, m, nullptr, true, W, d, T, c->stream));
+  int64_t count = (int64_t)m * d;
+  oja_elementwise_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, c->stream>>>(Q, T, W, vel, count, alpha, mu,
+                                                                                c->d_err);
+  PPCA_LAUNCH_CHECK(c, "oja_elementwise");
+  return PPCA_OK;
+}
+
+// EigenGame coefficients from A (m×m): Cf[j][i] = A_ji / A_ii (i < j), twoU[j] = 2(A_jj − Σ_{i<j} A_ji²/A_ii).
+__global__ void eg_coeff_kernel(const double* __restrict__ A, int m, double* __restrict__ Cf,
+                                double* __restrict__ twoU, int* d_err) {
+  __shared__ double amax;
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < m; ++i) mx = fmax(mx, A[i * m + i]);
+    amax = mx;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double u = A[j * m + j];
+    for (int i = 0; i < m; ++i) {
+      double cf = 0.0;
+      if (i < j) {
+        double aii = A[i * m + i];
+        if (!(aii > 1e-12 * amax)) {
+          atomicOr(d_err, DEV_DEGENERATE);
+          aii = 1.0;
+        }
+        cf = A[j * m + i] / aii;
+        u -= A[j * m + i] * cf;
+      }
+      Cf[j * m + i] = cf;
+    }
+    twoU[j] = 2.0 * u;
+  }
+}
+
+__global__ void eg_elementwise_kernel(const float* __restrict__ MV, const float* __restrict__ T,
+                                      const double* __restrict__ twoU, float* __restrict__ V,
+                                      float* __restrict__ vel, int64_t d, int64_t count, double alpha,
+                                      double mu, int* d_err) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  int64_t j = e / d;
+  double r = 2.0 * (double)MV[e] - 2.0 * (double)T[e] - twoU[j] * (double)V[e];
+  double v = mu * (double)vel[e] + r;
+  double w = (double)V[e] + alpha * (r + mu * v);
+  if (!isfinite(w)) atomicOr(d_err, DEV_NONFINITE);
+  vel[e] = (float)v;
+  V[e] = (float)w;
+}
+
+ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
+                             double alpha, double mu) {
+  double* Cf = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + (size_t)m * sizeof(double) + 64);
+  double* twoU = Cf + (size_t)m * m;
+  float* T = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
+  eg_coeff_kernel<<<1, 128, 0, c->stream>>>(A, m, Cf, twoU, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "eg_coeff");
+  PPCA_TRY(apply_rows(c, Cf, m, m, m, nullptr, false, MV, d, T, c->stream));
+  int64_t count = (int64_t)m * d;
+  eg_elementwise_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, c->stream>>>(MV, T, twoU, V, vel, d, count,
+                                                                               alpha, mu, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "eg_elementwise");
+  return normalize_rows(c, V, m, d);
+}
+
+// ============================================================================ eval dots
+__global__ void row_dots_kernel(const float* __restrict__ E, const float* __restrict__ T, int64_t d,
+                                double* __restrict__ out) {
+  const float* a = E + (int64_t)blockIdx.x * d;
+  const float* b = T + (int64_t)blockIdx.x * d;
+  double s = 0.0;
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) s += (double)a[x] * b[x];
+  s = warp_sum(s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[blockIdx.x] = t;
+  }
+}
+
+ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots) {
+  row_dots_kernel<<<k, 256, 0, c->stream>>>(E, T, d, dots);
+  PPCA_LAUNCH_CHECK(c, "row_dots");
+  return PPCA_OK;
+}
+
+}  // namespace ppca

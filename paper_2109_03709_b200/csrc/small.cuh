@@ -1,0 +1,42 @@
+// small.cuh — the m×m side of the hot path: vector Gram, Cholesky-QR re-orthonormalisation,
+// single-CTA fp64 Jacobi Rayleigh–Ritz, rotation, sign convention, priming updates.
+#pragma once
+#include "common.cuh"
+
+namespace ppca {
+
+// G[m][m] (fp64) = V Vᵀ for row vectors V [m][d] fp32 (partials in S_PART).
+ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G);
+
+// CholQR2 in place: W [m][d] ← Q-factor of the rows (positive diag R), twice.
+// drop_tol > 0: rows whose Cholesky pivot ≤ drop_tol²·G_jj are dropped (refine semantics,
+// SPEC L51); the survivors are compacted to the front, *m_out receives their count.
+// drop_tol == 0: any non-positive pivot flags SUBSPACE_COLLAPSE (power-iteration semantics).
+ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out);
+
+// Rayleigh–Ritz in one CTA (fp64): given S = (XWᵀ)ᵀ(XWᵀ) and Bm = WWᵀ of the operand rows,
+// solve S u = θ Bm u:  L = chol(Bm), Jacobi(L⁻¹SL⁻ᵀ) → θ (desc), U;  R = Uᵀ L⁻¹.
+// theta_dev: double[m]; R_dev: double[m][m] (row i lifts eigenvector i: e_i = Σ_j R_ij w_j).
+ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev,
+                       double* R_dev, cudaStream_t stream);
+
+// E[k][d] = R[:k] · W  (fp64 accumulate), then the sign convention on each row.
+ppca_status lift_rows(Ctx* c, const double* R, int ldr, const float* W, int m, int k, int64_t d,
+                      float* E, bool apply_sign, cudaStream_t stream);
+
+// W[c][j] = N(0,1) draw (seed, stream 6, c·d + j), rows scaled to unit norm.
+ppca_status init_rows(Ctx* c, uint64_t seed, float* W, int m, int64_t d);
+// rows scaled to unit norm (fp64 norms); flags DEGENERATE on a zero row.
+ppca_status normalize_rows(Ctx* c, float* W, int m, int64_t d);
+
+// Oja / Sanger update (fp64 per element):  G = Q − tril(P)·W;  v ← μv + G;  W ← W + α(G + μv).
+ppca_status oja_update(Ctx* c, const float* Q, const double* P, float* W, float* vel, int m,
+                       int64_t d, double alpha, double mu);
+// EigenGame update: coefficients from A, r = 2MV − 2 N·MV − 2U∘V, Nesterov, renormalise.
+ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m,
+                             int64_t d, double alpha, double mu);
+
+// dots[i] = <E_i, T_i> in fp64.
+ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots);
+
+}  // namespace ppca
