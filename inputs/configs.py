@@ -52,7 +52,7 @@ FULL = {w.name: w for w in (C1, C2, C3, C4, C5)}
 SMALL = {
     "C1": C1,
     "C2s": dataclasses.replace(C2, name="C2s", spec=dataclasses.replace(C2.spec, n=12_096), steps=200),
-    "C3s": dataclasses.replace(C3, name="C3s", spec=dataclasses.replace(C3.spec, n=20_011, d=256), iters=12),
+    "C3s": dataclasses.replace(C3, name="C3s", spec=dataclasses.replace(C3.spec, n=100_003, d=256), iters=12),
     "C4s": dataclasses.replace(C4, name="C4s", spec=dataclasses.replace(C4.spec, n=41_216, d=512),
                                batch=4096, steps=30),
     "C5s": dataclasses.replace(C5, name="C5s", spec=dataclasses.replace(C5.spec, n=6_007, d=2048), iters=8),

@@ -140,9 +140,11 @@ def matrix(X, n_global: int | None = None, layout: int = PPCA_LAYOUT_CONTIGUOUS,
     else:
         raise ValueError(f"unsupported dtype {X.dtype}")
     n_local = X.shape[0]
-    return ppca_matrix(int(X.data_ptr()), dt, n_local, n_global if n_global is not None else n_local,
-                       d if d is not None else X.shape[1], X.stride(0) if n_local > 0 else max(X.shape[1], 4),
-                       layout, block_rows)
+    mat = ppca_matrix(int(X.data_ptr()), dt, n_local, n_global if n_global is not None else n_local,
+                      d if d is not None else X.shape[1], X.stride(0) if n_local > 0 else max(X.shape[1], 4),
+                      layout, block_rows)
+    mat._tensor = X          # keep the device buffer alive as long as the descriptor
+    return mat
 
 
 def gen_spec(spec, layout: int = PPCA_LAYOUT_CONTIGUOUS, block_rows: int = 0) -> ppca_gen_spec:

@@ -18,6 +18,7 @@ namespace ppca {
 
 ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_t* n_local_out, double* mu_host);
 ppca_status philox_words(Ctx* c, uint64_t seed, uint32_t stream, uint64_t first, int64_t count, uint32_t* out);
+ppca_status debug_wait_counters(unsigned long long* out16);
 
 // ----------------------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
@@ -253,6 +254,9 @@ ppca_status ppca_get_pass_time(ppca_ctx* h, double* ms_total, int64_t* passes) {
   return pass_time_collect(&h->c, ms_total, passes);
 }
 
+// (undocumented, profiling) per-role mbarrier wait cycles of the tensor-core kernel A since last call
+ppca_status ppca_debug_wait_counters(unsigned long long* out16) { return ppca::debug_wait_counters(out16); }
+
 int ppca_last_pass_impl(const ppca_ctx* h) { return h ? h->c.last_impl : -1; }
 
 ppca_status ppca_set_pass_impl(ppca_ctx* h, int impl) {
@@ -322,7 +326,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     if (st == PPCA_OK) st = allreduce(c, S, (size_t)m * m, true);
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
-      st = vec_gram(c, W, m, d, Bm);
+      st = vec_gram(c, plan.Wop, m, d, Bm);
       if (st != PPCA_OK) break;
       cudaEventRecord(ev_main[t & 1], c->stream);
       cudaStreamWaitEvent(c->side, ev_main[t & 1], 0);
@@ -330,9 +334,8 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       cudaEventRecord(ev_side[t & 1], c->side);
       if (st != PPCA_OK) break;
     }
-    st = check_cuda(c, cudaMemcpyAsync(W, Z, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
-                    "copy Z");
-    if (st == PPCA_OK) st = cholqr2(c, W, m, d, 0.0, nullptr);
+    // W ← orth(Z): one fp64 Cholesky-QR pass (κ(Z)² ε64 ≪ fp32 rounding for power iterates)
+    st = cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
   }
   ppca_status st2 = finish(c, "ppca_prime_power");
   for (int i = 0; i < 2; ++i) {
@@ -433,9 +436,10 @@ ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m
   PPCA_TRY(pass_prepare(c, X, mm, &plan));
   PPCA_TRY(pass_gram(c, X, &plan, B, mm, S));            // S = (XBᵀ)ᵀ(XBᵀ)
   PPCA_TRY(allreduce(c, S, (size_t)mm * mm, true));
-  PPCA_TRY(vec_gram(c, B, mm, d, Bm));
+  const float* Bop = plan.Wop;                            // the operand rows the pass used
+  PPCA_TRY(vec_gram(c, Bop, mm, d, Bm));
   PPCA_TRY(ritz_solve(c, S, Bm, mm, theta_dev, R, c->stream));
-  PPCA_TRY(lift_rows(c, R, mm, B, mm, k, d, E, true, c->stream));
+  PPCA_TRY(lift_rows(c, R, mm, Bop, mm, k, d, E, true, c->stream));
   PPCA_TRY(finish(c, "ppca_refine"));
   if (theta_host && cudaMemcpy(theta_host, theta_dev, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
     return set_error(c, PPCA_ERR_CUDA, "copy theta");

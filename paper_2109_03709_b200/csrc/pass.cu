@@ -42,6 +42,8 @@ void pass_tc_release(Ctx* c);
 ppca_status pass_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan) {
   plan->impl = 1;
   if (c->pass_impl == 1) return PPCA_OK;
+  // auto: the tensor-core pass for HBM-sized shards; tiny problems stay on the exact-fp32 SIMT pass
+  if (c->pass_impl == 0 && X->n_local * X->d < (int64_t(1) << 24)) return PPCA_OK;
   ppca_status s = pass_tc_prepare(c, X, m, plan);
   if (s == PPCA_OK) return PPCA_OK;
   if (c->pass_impl == 2) return s;         // explicitly requested: report why it cannot run
@@ -76,12 +78,14 @@ static ppca_status pass_gram_impl(Ctx* c, const ppca_matrix* X, const PassPlan* 
 ppca_status pass_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S) {
   PassTimer t(c);
   c->last_impl = plan->impl;
+  const_cast<PassPlan*>(plan)->Wop = W;
   return pass_power_impl(c, X, plan, W, m, Z, S);
 }
 
 ppca_status pass_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S) {
   PassTimer t(c);
   c->last_impl = plan->impl;
+  const_cast<PassPlan*>(plan)->Wop = W;
   return pass_gram_impl(c, X, plan, W, m, S);
 }
 

@@ -8,6 +8,8 @@ namespace ppca {
 
 struct PassPlan {
   int impl = 1;
+  const float* Wop = nullptr;   // fp32 values of the operand rows the last pass actually used
+                                // (W itself for SIMT; RN_bf16(W) for tcgen05) — for the Ritz Gram
 };
 
 ppca_status pass_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan);

@@ -1,0 +1,170 @@
+// ritz.cuh — single-CTA fp64 Rayleigh–Ritz solve (§8 row a7; Alg. 1 step 4 "full-PCA"):
+//   S u = θ B u  with  B = L Lᵀ (Cholesky),  C = L⁻¹ S L⁻ᵀ,  C = U diag(θ) Uᵀ  (parallel cyclic Jacobi),
+//   R = Uᵀ L⁻¹  so that the lifted eigenvector i is  e_i = Σ_j R_ij w_j.
+// Jacobi uses the round-robin ("circle") pairing: m/2 disjoint rotations per round; A ← JᵀAJ is applied
+// block-wise — each (pair, pair) 2×2 block of A transforms independently — so a round costs two
+// barriers.  Convergence: off(A) ≤ 1e-12·‖diag A‖_F, at most 100 sweeps.
+// Shared memory: A (fp64) and V (fp64 for m ≤ 64, fp32 beyond) plus, for m ≤ 64, L⁻¹ and a temporary.
+#pragma once
+
+namespace ritz {
+
+__device__ __forceinline__ void pair_of(int r, int i, int mm, int& p, int& q) {
+  int a, b;
+  if (i == 0) {
+    a = 0;
+    b = (r % (mm - 1)) + 1;
+  } else {
+    a = ((i + r) % (mm - 1)) + 1;
+    b = ((mm - 1 - i + r) % (mm - 1)) + 1;
+  }
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S, const double* __restrict__ Bm, int m,
+                                                   double* __restrict__ gLinv, double* __restrict__ gT1,
+                                                   double* __restrict__ theta, double* __restrict__ R, int* d_err) {
+  extern __shared__ double sm[];
+  const int mm = (m + 1) & ~1;          // even (a dummy player for odd m)
+  const int np = mm / 2;
+  double* A = sm;                                     // mm × mm
+  VT* V = reinterpret_cast<VT*>(A + mm * mm);         // mm × mm
+  double* tail = reinterpret_cast<double*>(V + mm * mm + (sizeof(VT) == 4 && (mm * mm) % 2 ? 1 : 0));
+  const bool small = m <= 64;
+  double* Linv = small ? tail : gLinv;                // m × m
+  double* T1 = small ? tail + m * m : gT1;            // m × m
+  double* misc = small ? tail + 2 * m * m : tail;
+  double* diag0 = misc;                               // m
+  double* csn = diag0 + mm;                           // 2·np
+  int* keep = reinterpret_cast<int*>(csn + 2 * np);   // m
+  int* pq = keep + mm;                                // 2·np
+  int* perm = pq + 2 * np;                            // m
+  __shared__ double red[2][16];
+  __shared__ int converged;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  // 1. L = chol(B) (in A), L⁻¹
+  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
+  __syncthreads();
+  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err);
+  ppca::block_lower_inverse(A, m, keep, Linv);
+  // 2. C = L⁻¹ S L⁻ᵀ  (T1 = S L⁻ᵀ, then A = L⁻¹ T1), stored mm × mm with a zero dummy row/column
+  for (int e = tid; e < m * m; e += nt) {            // lanes vary i: Linv[j][·] is a broadcast
+    const int j = e / m, i = e % m;
+    double s = 0.0;
+    for (int t = 0; t <= j; ++t) s += S[i * m + t] * Linv[j * m + t];
+    T1[i * m + j] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * mm; e += nt) {
+    const int i = e / mm, j = e % mm;
+    double s = 0.0;
+    if (i < m && j < m)
+      for (int t = 0; t <= i; ++t) s += Linv[i * m + t] * T1[t * m + j];
+    A[e] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * mm; e += nt) {
+    const int i = e / mm, j = e % mm;
+    if (i < j) {
+      const double v = 0.5 * (A[i * mm + j] + A[j * mm + i]);
+      A[i * mm + j] = v;
+      A[j * mm + i] = v;
+    }
+    V[e] = (VT)(i == j ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  // 3. Jacobi sweeps
+  for (int sweep = 0; sweep <= 100; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int e = tid; e < mm * mm; e += nt) {
+      const double v = A[e];
+      if (e / mm == e % mm) dg += v * v; else off += v * v;
+    }
+    off = ppca::warp_sum(off);
+    dg = ppca::warp_sum(dg);
+    if ((tid & 31) == 0) { red[0][tid >> 5] = off; red[1][tid >> 5] = dg; }
+    __syncthreads();
+    if (tid == 0) {
+      double o = 0, g = 0;
+      for (int w = 0; w < nt / 32; ++w) { o += red[0][w]; g += red[1][w]; }
+      converged = (sqrt(o) <= 1e-12 * sqrt(g)) || o == 0.0;
+      if (!converged && sweep == 100) atomicOr(d_err, ppca::DEV_NOCONV);
+    }
+    __syncthreads();
+    if (converged || sweep == 100) break;
+    for (int r = 0; r < mm - 1; ++r) {
+      for (int i = tid; i < np; i += nt) {
+        int p, q;
+        pair_of(r, i, mm, p, q);
+        double cc = 1.0, ss = 0.0;
+        const double apq = A[p * mm + q];
+        if (apq != 0.0) {
+          const double tau = (A[q * mm + q] - A[p * mm + p]) / (2.0 * apq);
+          const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          cc = 1.0 / sqrt(1.0 + t * t);
+          ss = t * cc;
+        }
+        pq[2 * i] = p;
+        pq[2 * i + 1] = q;
+        csn[2 * i] = cc;
+        csn[2 * i + 1] = ss;
+      }
+      __syncthreads();
+      // A ← JᵀAJ one (pair a, pair b) 2×2 block at a time; V ← VJ one (row, pair) couple at a time
+      for (int e = tid; e < np * np; e += nt) {
+        const int ia = e / np, ib = e % np;
+        const int p = pq[2 * ia], q = pq[2 * ia + 1], p2 = pq[2 * ib], q2 = pq[2 * ib + 1];
+        const double c1 = csn[2 * ia], s1 = csn[2 * ia + 1], c2 = csn[2 * ib], s2 = csn[2 * ib + 1];
+        const double a = A[p * mm + p2], b = A[p * mm + q2], c = A[q * mm + p2], d = A[q * mm + q2];
+        // rows:  p ← c1·p − s1·q,  q ← s1·p + c1·q ;  columns: p2 ← c2·p2 − s2·q2, q2 ← s2·p2 + c2·q2
+        const double ra = c1 * a - s1 * c, rb = c1 * b - s1 * d, rc = s1 * a + c1 * c, rd = s1 * b + c1 * d;
+        A[p * mm + p2] = c2 * ra - s2 * rb;
+        A[p * mm + q2] = s2 * ra + c2 * rb;
+        A[q * mm + p2] = c2 * rc - s2 * rd;
+        A[q * mm + q2] = s2 * rc + c2 * rd;
+      }
+      for (int e = tid; e < np * mm; e += nt) {        // V stored transposed: V[col·mm + row]
+        const int ia = e / mm, row = e % mm;
+        const int p = pq[2 * ia], q = pq[2 * ia + 1];
+        const double cc = csn[2 * ia], ss = csn[2 * ia + 1];
+        const double vp = (double)V[p * mm + row], vq = (double)V[q * mm + row];
+        V[p * mm + row] = (VT)(cc * vp - ss * vq);
+        V[q * mm + row] = (VT)(ss * vp + cc * vq);
+      }
+      __syncthreads();
+    }
+  }
+  // 4. sort descending (ties by index), R = U_sortedᵀ L⁻¹
+  for (int i = tid; i < m; i += nt) {
+    const double li = A[i * mm + i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      const double lj = A[j * mm + j];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += nt) theta[i] = A[perm[i] * mm + perm[i]];
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    const int col = perm[i];
+    double s = 0.0;
+    for (int t = j; t < m; ++t) s += (double)V[col * mm + t] * Linv[t * m + j];
+    R[e] = s;
+  }
+}
+
+inline size_t smem_bytes(int m) {
+  const int mm = (m + 1) & ~1;
+  const bool small = m <= 64;
+  size_t b = (size_t)mm * mm * 8 + (size_t)mm * mm * (small ? 8 : 4) + 8;
+  if (small) b += (size_t)2 * m * m * 8;
+  b += (size_t)mm * 8 + (size_t)mm * 8 + (size_t)mm * 4 + (size_t)mm * 4 + (size_t)mm * 4 + 64;
+  return b;
+}
+
+}  // namespace ritz

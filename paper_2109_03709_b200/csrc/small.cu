@@ -62,6 +62,7 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
   __syncthreads();
   __shared__ double piv;
   __shared__ int dropped;
+  __shared__ double colj[PPCA_MAX_M];    // column j of L (row-contiguous copy: no 32-way bank conflicts)
   for (int j = 0; j < m; ++j) {
     if (tid == 0) {
       double p = A[j * m + j];
@@ -82,12 +83,16 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
       __syncthreads();
       continue;
     }
-    for (int i = j + tid; i < m; i += nt) A[i * m + j] = (i == j) ? piv : A[i * m + j] / piv;
+    for (int i = j + tid; i < m; i += nt) {
+      const double v = (i == j) ? piv : A[i * m + j] / piv;
+      A[i * m + j] = v;
+      colj[i] = v;
+    }
     __syncthreads();
     const int rem = m - j - 1;
     for (int e = tid; e < rem * rem; e += nt) {
       int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) A[i * m + k] -= A[i * m + j] * A[k * m + j];
+      if (k <= i) A[i * m + k] -= colj[i] * colj[k];
     }
     __syncthreads();
   }
@@ -115,10 +120,17 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
   double* A = sm;                                  // m*m
   double* diag0 = A + m * m;                       // m
   int* keep = (int*)(diag0 + m);                   // m
+  double* Ls = reinterpret_cast<double*>(keep + ((m + 1) & ~1));   // m*m when m ≤ 90 (L⁻¹ built in smem)
+  const bool in_smem = m <= 90;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) A[e] = G[e];
   __syncthreads();
   block_cholesky(A, m, drop, keep, diag0, d_err);
-  block_lower_inverse(A, m, keep, Linv);
+  if (in_smem) {
+    block_lower_inverse(A, m, keep, Ls);
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) Linv[e] = Ls[e];
+  } else {
+    block_lower_inverse(A, m, keep, Linv);
+  }
   if (threadIdx.x == 0) {
     int o = 0;
     for (int i = 0; i < m; ++i) row_map[i] = keep[i] ? o++ : -1;
@@ -133,18 +145,23 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
                                                          int64_t d, float* __restrict__ OUT) {
-  extern __shared__ double cs[];                 // rows * m_in
-  for (int e = threadIdx.x; e < rows * m_in; e += blockDim.x) cs[e] = C[(int64_t)(e / m_in) * ldc + e % m_in];
+  extern __shared__ double cs[];                 // 8 rows × m_in (this block's output rows)
+  const int r0 = blockIdx.y * 8;
+  const int nr = min(8, rows - r0);
+  for (int e = threadIdx.x; e < nr * m_in; e += blockDim.x)
+    cs[e] = C[(int64_t)(r0 + e / m_in) * ldc + e % m_in];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t x0 = (int64_t)blockIdx.x * 128 + lane;
-  for (int i = warp; i < rows; i += 8) {
+  if (warp < nr) {
+    const int i = r0 + warp;
+    const double* crow = cs + warp * m_in;
     int oi = row_map ? row_map[i] : i;
-    if (oi < 0) continue;
+    if (oi < 0) return;
     double acc[4] = {0, 0, 0, 0};
     int jend = lower ? i + 1 : m_in;
     for (int j = 0; j < jend; ++j) {
-      double cij = cs[i * m_in + j];
+      double cij = crow[j];
       if (cij == 0.0) continue;
       const float* in = IN + (int64_t)j * d;
 #pragma unroll
@@ -163,20 +180,22 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
 
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
                               bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  size_t smem = (size_t)rows * m_in * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  apply_rows_kernel<<<(unsigned)ceil_div(d, 128), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN,
-                                                                  d, OUT);
+  size_t smem = (size_t)8 * m_in * sizeof(double);
+  dim3 grid((unsigned)ceil_div(d, 128), (unsigned)ceil_div(rows, 8));
+  apply_rows_kernel<<<grid, 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
 
 // ============================================================================ CholQR2
 ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out) {
+  return cholqr(c, W, W, m, d, drop_tol, m_out, 2);
+}
+
+// W = Q-factor of the rows of Zin (positive diag R).  One pass is exact up to ε64·κ(Zin)² in fp64
+// (the Gram, Cholesky and apply are fp64); a second pass restores orthonormality for ill-conditioned
+// inputs (the refine path).
+ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes) {
   double* G = (double*)scratch(c, S_GRAM, (size_t)m * m * sizeof(double));
   double* Linv = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64);
   int* row_map = (int*)(Linv + (size_t)m * m);
@@ -188,8 +207,20 @@ ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + m * sizeof(int);
-  for (int pass = 0; pass < 2; ++pass) {
+  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + ((m + 1) & ~1) * sizeof(int) +
+                (m <= 90 ? (size_t)m * m * sizeof(double) : 0);
+  if (Zin != W && passes == 1 && drop_tol <= 0.0) {
+    PPCA_TRY(vec_gram(c, Zin, m, d, G));
+    chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
+    PPCA_LAUNCH_CHECK(c, "chol_inv");
+    PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, Zin, d, W, c->stream));
+    if (m_out) *m_out = m;
+    return PPCA_OK;
+  }
+  if (Zin != W)
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(W, Zin, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                        "copy Z"));
+  for (int pass = 0; pass < passes; ++pass) {
     PPCA_TRY(vec_gram(c, W, m, d, G));
     chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, pass == 0 ? drop_tol : 0.0, Linv, row_map, d_mout,
                                                  c->d_err);
@@ -216,168 +247,23 @@ ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_
 }
 
 // ============================================================================ Rayleigh–Ritz (one CTA)
-__device__ __forceinline__ void jacobi_pair(int r, int i, int mm, int& p, int& q) {
-  // circle method: player 0 fixed, players 1..mm-1 rotate; position j holds ((j + r) % (mm-1)) + 1
-  int a, b;
-  if (i == 0) {
-    a = 0;
-    b = (r % (mm - 1)) + 1;
-  } else {
-    a = ((i + r) % (mm - 1)) + 1;
-    b = ((mm - 1 - i + r) % (mm - 1)) + 1;
-  }
-  p = a < b ? a : b;
-  q = a < b ? b : a;
-}
-
-// smem: A[m*m] (fp64) + small arrays.  Global scratch: Linv[m*m], Vg[m*m], T1[m*m].
-__global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
-                                                   int m, double* __restrict__ Linv, double* __restrict__ Vg,
-                                                   double* __restrict__ T1, double* __restrict__ theta,
-                                                   double* __restrict__ R, int* d_err) {
-  extern __shared__ double sm[];
-  double* A = sm;                       // m*m
-  double* diag0 = A + m * m;            // m
-  double* csn = diag0 + m;              // 2 * 64 (c, s) for up to 64 pairs
-  int* keep = (int*)(csn + 2 * (PPCA_MAX_M / 2 + 1));
-  int* pq = keep + m;                   // 2 * pairs
-  int* perm = pq + 2 * (PPCA_MAX_M / 2 + 1);
-  __shared__ double red[2][32];
-  __shared__ int converged;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  // 1. L = chol(Bm), Linv
-  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
-  __syncthreads();
-  block_cholesky(A, m, 0.0, keep, diag0, d_err);
-  block_lower_inverse(A, m, keep, Linv);
-  // 2. C = Linv · S · Linvᵀ :  T1 = S · Linvᵀ  then  A = Linv · T1
-  for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, j = e % m;
-    double s = 0.0;
-    for (int t = 0; t <= j; ++t) s += S[i * m + t] * Linv[(int64_t)j * m + t];
-    T1[e] = s;
-  }
-  __syncthreads();
-  for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, j = e % m;
-    double s = 0.0;
-    for (int t = 0; t <= i; ++t) s += Linv[(int64_t)i * m + t] * T1[t * m + j];
-    A[e] = s;
-  }
-  __syncthreads();
-  // symmetrise
-  for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, j = e % m;
-    if (i < j) {
-      double v = 0.5 * (A[i * m + j] + A[j * m + i]);
-      A[i * m + j] = v;
-      A[j * m + i] = v;
-    }
-  }
-  for (int e = tid; e < m * m; e += nt) Vg[e] = (e / m == e % m) ? 1.0 : 0.0;
-  __syncthreads();
-  // 3. parallel cyclic Jacobi (circle ordering), ≤ 100 sweeps, off < 1e-12·‖diag‖
-  const int mm = (m + 1) & ~1;
-  const int npairs = mm / 2;
-  for (int sweep = 0; sweep <= 100; ++sweep) {
-    double off = 0.0, dg = 0.0;
-    for (int e = tid; e < m * m; e += nt) {
-      double v = A[e];
-      if (e / m == e % m) dg += v * v; else off += v * v;
-    }
-    off = warp_sum(off);
-    dg = warp_sum(dg);
-    if ((tid & 31) == 0) { red[0][tid >> 5] = off; red[1][tid >> 5] = dg; }
-    __syncthreads();
-    if (tid == 0) {
-      double o = 0, g = 0;
-      for (int w = 0; w < nt / 32; ++w) { o += red[0][w]; g += red[1][w]; }
-      converged = (sqrt(o) <= 1e-12 * sqrt(g)) || o == 0.0;
-      if (!converged && sweep == 100) atomicOr(d_err, DEV_NOCONV);
-    }
-    __syncthreads();
-    if (converged || sweep == 100) break;
-    for (int r = 0; r < mm - 1; ++r) {
-      for (int i = tid; i < npairs; i += nt) {
-        int p, q;
-        jacobi_pair(r, i, mm, p, q);
-        double cc = 1.0, ss = 0.0;
-        if (q < m) {
-          double apq = A[p * m + q];
-          if (apq != 0.0) {
-            double tau = (A[q * m + q] - A[p * m + p]) / (2.0 * apq);
-            double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            cc = 1.0 / sqrt(1.0 + t * t);
-            ss = t * cc;
-          }
-        }
-        pq[2 * i] = p;
-        pq[2 * i + 1] = q;
-        csn[2 * i] = cc;
-        csn[2 * i + 1] = ss;
-      }
-      __syncthreads();
-      // columns of A and V:  (x_p, x_q) ← (c x_p − s x_q, s x_p + c x_q)
-      for (int e = tid; e < npairs * m; e += nt) {
-        int i = e / m, row = e % m;
-        int p = pq[2 * i], q = pq[2 * i + 1];
-        double cc = csn[2 * i], ss = csn[2 * i + 1];
-        if (q >= m || ss == 0.0) continue;
-        double ap = A[row * m + p], aq = A[row * m + q];
-        A[row * m + p] = cc * ap - ss * aq;
-        A[row * m + q] = ss * ap + cc * aq;
-        double vp = Vg[row * m + p], vq = Vg[row * m + q];
-        Vg[row * m + p] = cc * vp - ss * vq;
-        Vg[row * m + q] = ss * vp + cc * vq;
-      }
-      __syncthreads();
-      // rows of A
-      for (int e = tid; e < npairs * m; e += nt) {
-        int i = e / m, col = e % m;
-        int p = pq[2 * i], q = pq[2 * i + 1];
-        double cc = csn[2 * i], ss = csn[2 * i + 1];
-        if (q >= m || ss == 0.0) continue;
-        double ap = A[p * m + col], aq = A[q * m + col];
-        A[p * m + col] = cc * ap - ss * aq;
-        A[q * m + col] = ss * ap + cc * aq;
-      }
-      __syncthreads();
-    }
-  }
-  // 4. sort descending (ties by index) and R = U_sortedᵀ · Linv
-  for (int i = tid; i < m; i += nt) {
-    double li = A[i * m + i];
-    int rank = 0;
-    for (int j = 0; j < m; ++j) {
-      double lj = A[j * m + j];
-      rank += (lj > li) || (lj == li && j < i);
-    }
-    perm[rank] = i;
-  }
-  __syncthreads();
-  for (int i = tid; i < m; i += nt) theta[i] = A[perm[i] * m + perm[i]];
-  for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, j = e % m;          // R[i][j] = Σ_t V[t][perm i] Linv[t][j]
-    int col = perm[i];
-    double s = 0.0;
-    for (int t = j; t < m; ++t) s += Vg[t * m + col] * Linv[(int64_t)t * m + j];
-    R[e] = s;
-  }
-}
+#include "ritz.cuh"
 
 ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev, double* R_dev,
                        cudaStream_t stream) {
-  double* scr = (double*)scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double));
+  double* scr = (double*)scratch(c, S_EVAL, (size_t)2 * m * m * sizeof(double));
   if (!scr) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(ritz::ritz_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + 2 * (PPCA_MAX_M / 2 + 1) * sizeof(double) +
-                (size_t)m * sizeof(int) + 2 * (PPCA_MAX_M / 2 + 1) * sizeof(int) + PPCA_MAX_M * sizeof(int);
-  ritz_kernel<<<1, 512, smem, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, scr + (size_t)2 * m * m, theta_dev,
-                                        R_dev, c->d_err);
+  const size_t smem = ritz::smem_bytes(m);
+  if (m <= 64)
+    ritz::ritz_kernel<double><<<1, 512, smem, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, R_dev, c->d_err);
+  else
+    ritz::ritz_kernel<float><<<1, 512, smem, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, R_dev, c->d_err);
   PPCA_LAUNCH_CHECK(c, "ritz_kernel");
   return PPCA_OK;
 }

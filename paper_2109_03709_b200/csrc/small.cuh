@@ -13,6 +13,8 @@ ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G);
 // SPEC L51); the survivors are compacted to the front, *m_out receives their count.
 // drop_tol == 0: any non-positive pivot flags SUBSPACE_COLLAPSE (power-iteration semantics).
 ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out);
+// General form: W (may alias Zin) = orth(Zin) with `passes` Cholesky-QR passes.
+ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes);
 
 // Rayleigh–Ritz in one CTA (fp64): given S = (XWᵀ)ᵀ(XWᵀ) and Bm = WWᵀ of the operand rows,
 // solve S u = θ Bm u:  L = chol(Bm), Jacobi(L⁻¹SL⁻ᵀ) → θ (desc), U;  R = Uᵀ L⁻¹.
