@@ -136,7 +136,7 @@ def oracle_step_rate(w, rows: int, steps: int, warmup: int = 0):
 def run_reference(args, w, rank):
     if rank != 0:
         return 0
-    rows = args.ref_rows or min(w.spec.n, 65536)
+    rows = args.ref_rows or min(w.spec.n, 65536, (1 << 30) // (8 * w.spec.d))
     gbs, dt = oracle_step_rate(w, rows, max(1, args.steps), max(0, min(args.warmup, 1)))
     cores = os.cpu_count()
     sample = f"{rows} of {w.spec.n} rows of {w.name}; fp64 numpy oracle power step (Y=XWᵀ, Z=YᵀX, S=YᵀY, GS) + eig(S)"
@@ -160,19 +160,12 @@ def run_ours(args, w, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream()
-    uid = None
-    if world > 1:
-        t = torch.zeros(P.PPCA_UNIQUE_ID_BYTES, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(P.ppca_get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().numpy().tobytes())
-    ctx = P.ppca_ctx_create(local_rank, stream, uid, rank, world)
+    ctx = P.ppca_ctx_create_distributed(local_rank, stream)
     impl_code = {"auto": 0, "simt": 1, "tc": 2}[args.pass_impl]
     P.ppca_set_pass_impl(ctx, impl_code)
     s = w.spec
     per = -(-s.n // world)
-    n_local = max(0, min(s.n, per * (rank + 1)) - min(s.n, per * rank))
+    _, n_local = P.contiguous_shard(s.n, rank, world)
     dt = torch.float32 if s.dtype == "f32" else torch.bfloat16
     elt = 4 if s.dtype == "f32" else 2
     X = torch.empty((max(n_local, 1), s.d), dtype=dt, device=dev)[:n_local]
@@ -279,7 +272,7 @@ def run_ours(args, w, rank, world, local_rank):
         return 0
     cpu = None
     if world == 1 and not args.no_cpu:
-        rows = args.cpu_rows or min(s.n, 131072)
+        rows = args.cpu_rows or min(s.n, 131072, (1 << 30) // (8 * s.d))   # ≤ 1 GiB of fp64 sample
         gbs, dt_s = oracle_step_rate(w, rows, 2, 0)
         cpu = {"value": gbs, "unit": "GB/s", "cores": os.cpu_count(), "kind": "oracle",
                "sample": f"{rows} of {s.n} rows of {w.name}, 2 fp64 numpy oracle power steps "

@@ -156,6 +156,40 @@ def gen_spec(spec, layout: int = PPCA_LAYOUT_CONTIGUOUS, block_rows: int = 0) ->
                          PPCA_F32 if spec.dtype == "f32" else PPCA_BF16, spec.n, spec.d, spec.seed, layout, block_rows)
 
 
+# ----------------------------------------------------------------------------- multi-GPU plumbing
+def contiguous_shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """(first row, rows) of rank's CONTIGUOUS shard: rows [⌈n/G⌉·g, min(n, ⌈n/G⌉·(g+1))) (ppca.h)."""
+    per = -(-n // world)
+    r0 = min(n, per * rank)
+    return r0, max(0, min(n, per * (rank + 1)) - r0)
+
+
+def broadcast_unique_id(uid: bytes | None, group=None) -> bytes:
+    """Rank 0's NCCL unique id (PPCA_UNIQUE_ID_BYTES bytes) delivered to every rank through the
+    active torch.distributed process group (device tensor for nccl, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.zeros(PPCA_UNIQUE_ID_BYTES, dtype=torch.uint8, device=dev)
+    if dist.get_rank(group) == 0:
+        if uid is None or len(uid) != PPCA_UNIQUE_ID_BYTES:
+            raise ValueError("rank 0 must provide a PPCA_UNIQUE_ID_BYTES unique id")
+        t.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
+    dist.broadcast(t, 0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def ppca_ctx_create_distributed(local_rank: int, stream=None):
+    """Collective: one context per rank of the active torch.distributed group (NCCL comm of the
+    library bootstrapped from rank 0's unique id); world == 1 creates a plain context."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return ppca_ctx_create(local_rank, stream)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    uid = broadcast_unique_id(ppca_get_unique_id() if rank == 0 else None)
+    return ppca_ctx_create(local_rank, stream, uid, rank, world)
+
+
 # ----------------------------------------------------------------------------- ABI (same names)
 def ppca_status_string(s: int) -> str:
     return load().ppca_status_string(s).decode()

@@ -316,6 +316,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     cudaEventRecord(ev_side[i], c->side);
   }
   ppca_status st = PPCA_OK;
+  c->side_busy = theta_hist_host != nullptr;
   for (int t = 0; t < iters && st == PPCA_OK; ++t) {
     double* S = Sbuf + (size_t)(t & 1) * m * m;
     double* Bm = Sbuf + (size_t)(2 + (t & 1)) * m * m;
@@ -337,6 +338,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     // W ← orth(Z): one fp64 Cholesky-QR pass (κ(Z)² ε64 ≪ fp32 rounding for power iterates)
     st = cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
   }
+  c->side_busy = false;
   ppca_status st2 = finish(c, "ppca_prime_power");
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(ev_main[i]);

@@ -30,6 +30,8 @@ struct Ctx {
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // side stream (Ritz solves overlap the next pass)
+  bool side_busy = false;             // side-stream kernels may overlap the next pass: persistent
+                                      // pass kernels then leave one SM free (a late CTA stalls the pass)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   void* nccl_comm = nullptr;          // ncclComm_t when world > 1
   int* d_err = nullptr;               // device error word

@@ -157,6 +157,10 @@ struct TcState {
 
 static int pad16(int m) { return (m + 15) & ~15; }
 
+// one CTA per SM; one SM is left free while side-stream work (the Ritz solve of the previous
+// iterate) may be resident, otherwise the CTA queued behind it delays the whole persistent pass
+static int persistent_ctas(const Ctx* c) { return c->side_busy ? c->sm_count - 1 : c->sm_count; }
+
 template <int MP, bool XBF16>
 static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const KAParams& kp, int grid) {
   const size_t smem = ka::smem_bytes(MP, XBF16);
@@ -248,7 +252,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   static int dbg = -1;
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   kp.dbg = dbg;
-  int grid = (int)std::min<int64_t>(c->sm_count, kp.ntiles);
+  int grid = (int)std::min<int64_t>(persistent_ctas(c), kp.ntiles);
   double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * mp * mp * sizeof(double));
   if (!Spart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   kp.Spart = Spart;
@@ -284,7 +288,8 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   KBParams bp;
   bp.X = X->data; bp.n = n; bp.d = d; bp.ld = X->ld; bp.m = m; bp.mp = mp;
   bp.ndg = ceil_div(d, nc * 128);
-  int64_t want = std::max<int64_t>(1, ceil_div(4 * (int64_t)c->sm_count, bp.ndg));
+  const int64_t ctas = persistent_ctas(c);
+  int64_t want = std::max<int64_t>(1, ceil_div(4 * ctas, bp.ndg));
   int64_t rpg = ceil_div(ceil_div(n, want), kb::KR) * kb::KR;
   rpg = std::max<int64_t>(rpg, kb::KR);
   bp.rows_per_rg = rpg;
@@ -300,7 +305,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   } else {
     tmX = tmYT;
   }
-  const int grid = (int)std::min<int64_t>(c->sm_count, bp.ndg * bp.nrg);
+  const int grid = (int)std::min<int64_t>(ctas, bp.ndg * bp.nrg);
   PPCA_TRY(X->dtype == PPCA_BF16 ? dispatch_kb<true>(c, mp, tmYT, tmX, bp, grid) : dispatch_kb<false>(c, mp, tmYT, tmX, bp, grid));
   reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");

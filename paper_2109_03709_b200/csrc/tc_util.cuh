@@ -76,6 +76,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// L2 prefetch of the line holding p (no register, no scoreboard: converters run it several chunks ahead
+// of their loads so those hit L2 instead of waiting a full DRAM latency)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ----------------------------------------------------------------------------- TMEM
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result) {   // one full warp

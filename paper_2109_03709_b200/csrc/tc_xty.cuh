@@ -12,6 +12,7 @@ namespace kb {
 constexpr int KR = 64;          // rows (K) per stage
 constexpr int NST = 4;
 constexpr int NCONV = 8;
+constexpr int PF = 0;           // converter L2-prefetch distance in half-stages (measured: hurts; off)
 constexpr int W_CONV0 = 4, W_PROD = 12, W_MMA = 13;
 constexpr int NTHREADS = 14 * 32;
 constexpr uint32_t BLK = KR * 128;            // one 64-column block of a stage (bytes)
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int64_t nitems = p.ndg * p.nrg;
   auto item_rows = [&](int64_t item, int64_t& r0, int64_t& nks) {
-    const int64_t rg = item % p.nrg;
+    const int64_t rg = item / p.ndg;      // CTAs working concurrently share a row group: Yᵀ hits L2
     r0 = rg * p.rows_per_rg;
     const int64_t r1 = min(p.n, r0 + p.rows_per_rg);
     nks = r1 > r0 ? (r1 - r0 + KR - 1) / KR : 0;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
       for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         int64_t r0, nks;
         item_rows(item, r0, nks);
-        const int64_t c0 = (item / p.nrg) * (NC * 128);
+        const int64_t c0 = (item % p.ndg) * (NC * 128);
         for (int64_t ks = 0; ks < nks; ++ks, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -166,8 +167,30 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
         }
         return true;
       };
+      // L2 prefetch PF half-stages ahead (a second cursor over the same sequence; one prefetch per line)
+      int64_t pf_item = cur_item, pf_ks = 0, pf_r0 = cur_r0, pf_nks = cur_nks;
+      int pf_h = 0;
+      auto prefetch_next = [&]() {
+        while (pf_item < nitems && pf_ks >= pf_nks) {
+          pf_item += gridDim.x;
+          pf_ks = 0;
+          if (pf_item < nitems) item_rows(pf_item, pf_r0, pf_nks);
+        }
+        if (pf_item >= nitems) return;
+        const int64_t c0 = (pf_item % p.ndg) * (NC * 128);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int f = (i * NCONV + cw) * 32 + lane;
+          const int row = f / (NC * 32), c4 = f % (NC * 32);
+          const int64_t r = pf_r0 + pf_ks * KR + pf_h * (KR / 2) + row, col = c0 + c4 * 4;
+          if ((c4 & 7) == 0 && r < p.n && col < p.d) prefetch_l2(X + r * p.ld + col);
+        }
+        if (++pf_h == 2) { pf_h = 0; ++pf_ks; }
+      };
+      for (int i = 0; i < PF; ++i) prefetch_next();
       auto load = [&](const Pos& q, float4 (&r)[PER]) {
-        const int64_t c0 = (q.item / p.nrg) * (NC * 128);
+        if (PF) prefetch_next();
+        const int64_t c0 = (q.item % p.ndg) * (NC * 128);
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
           const int f = (i * NCONV + cw) * 32 + lane;             // float4 index within the half-stage
@@ -212,7 +235,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++tt) {
       int64_t r0, nks;
       item_rows(item, r0, nks);
-      const int64_t dg = item / p.nrg, rg = item % p.nrg;
+      const int64_t dg = item % p.ndg, rg = item / p.ndg;
       const uint32_t b = tt & 1, tph = (tt >> 1) & 1;
       mbar_wait(&tfull[b], tph);
       tc_fence_after();
