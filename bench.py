@@ -171,8 +171,17 @@ def run_ours(args, w, rank, world, local_rank):
     X = torch.empty((max(n_local, 1), s.d), dtype=dt, device=dev)[:n_local]
     t0 = time.time()
     P.ppca_generate(ctx, P.gen_spec(s), X if n_local else torch.empty((0, s.d), dtype=dt, device=dev))
+    torch.cuda.synchronize()
     gen_s = time.time() - t0
-    Xm = P.matrix(X, n_global=s.n, d=s.d)
+    # fp32 data is held in the tensor-core-native split layout (include/ppca.h PPCA_F32_SPLIT): same bytes
+    split = s.dtype == "f32" and args.storage == "split"
+    Xh = None
+    if split:
+        if not args.no_e2e and n_local > 0:
+            Xh = torch.empty(X.shape, dtype=dt, pin_memory=True)      # the user's fp32 rows, for e2e
+            Xh.copy_(X)
+        P.ppca_split_f32(ctx, X, s.d)
+    Xm = P.matrix(X, n_global=s.n, d=s.d, split=split)
     W = torch.empty((w.m, s.d), dtype=torch.float32, device=dev)
     P.ppca_prime_power(ctx, Xm, w.m, 0, w.init_seed, W)             # W_0
     P.ppca_prime_power(ctx, Xm, w.m, args.warmup, 0, W, theta_hist=True)
@@ -219,15 +228,18 @@ def run_ours(args, w, rank, world, local_rank):
     # ---------------- end to end through the ABI with host buffers (H2D of X + D2H of θ every step)
     e2e = None
     if not args.no_e2e and n_local > 0:
-        Xh = torch.empty(X.shape, dtype=dt, pin_memory=True)
-        Xh.copy_(X)
+        if Xh is None:
+            Xh = torch.empty(X.shape, dtype=dt, pin_memory=True)
+            Xh.copy_(X)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ke = max(1, min(args.steps, 5))
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(ke):
-            X.copy_(Xh, non_blocking=True)
+            X.copy_(Xh, non_blocking=True)                             # the user's fp32 rows
+            if split:
+                P.ppca_split_f32(ctx, X, s.d)                             # → split layout (in place)
             P.ppca_prime_power(ctx, Xm, w.m, 1, 0, W, theta_hist=True)   # θ read back to the host
         e1.record(stream)
         torch.cuda.synchronize()
@@ -285,6 +297,7 @@ def run_ours(args, w, rank, world, local_rank):
         "config": {"workload": f"{w.name} (BASELINE.json configs[2]): planted exp spectrum, n={s.n}, d={s.d}, "
                                f"{s.dtype}, k={w.k}, l={w.l}, block power priming",
                    "n": s.n, "d": s.d, "m": w.m, "k": w.k, "priming": w.priming, "pass_impl": plan_impl,
+                   "storage": "f32 split (bf16 hi/lo planes, 4 B/elt)" if split else s.dtype,
                    "parallelism": f"dp{world} (contiguous row shards, NCCL all-reduce of Z,S)",
                    "l2": f"inputs larger than L2 (X shard {per_rank_bytes / 1e9:.2f} GB vs 126 MB L2)",
                    "step": "pass + allreduce + CholQR2 + fp64 Rayleigh-Ritz of S"},
@@ -311,6 +324,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--pass-impl", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--storage", default="split", choices=["split", "f32"],
+                    help="layout of fp32 X in HBM (split = PPCA_F32_SPLIT, the default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lces", action="store_true")

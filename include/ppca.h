@@ -50,7 +50,15 @@ typedef enum {
   PPCA_ERR_UNSUPPORTED = 10          /* not an sm_100 device, NCCL missing for world > 1, ... */
 } ppca_status;
 
-typedef enum { PPCA_F32 = 0, PPCA_BF16 = 1 } ppca_dtype;
+/* Storage of X.  PPCA_F32_SPLIT is the tensor-core-native layout of fp32 data: each fp32 value x is
+ * held as the round-to-nearest bf16 pair hi = RN(x), lo = RN(x − hi) (x − (hi + lo) ≤ 2^-17·|x|,
+ * unbiased), and row r of a shard [n_local][ld] (ld in 4-byte logical elements, ld ≥ d) holds the d hi
+ * values followed by the d lo values (2·d bf16 = 4·d bytes, so the row is exactly as long as its fp32
+ * form; d % 8 == 0 keeps the lo plane 16-byte aligned).  TMA stages both planes straight into the
+ * UMMA swizzle and the X·Wᵀ product reads X_hi + X_lo, while the Xᵀ·Y product reads only the hi plane
+ * (DESIGN.md §5), so no CUDA-core conversion runs per pass.  ppca_split_f32 converts fp32 rows in
+ * place; ppca_generate writes it directly. */
+typedef enum { PPCA_F32 = 0, PPCA_BF16 = 1, PPCA_F32_SPLIT = 2 } ppca_dtype;
 
 /* Row layout of a shard.  CONTIGUOUS: rank g holds global rows [⌈n/G⌉g, ⌈n/G⌉(g+1)).
  * INTERLEAVED: every minibatch block of block_rows rows (the last one may be shorter, size p)
@@ -113,10 +121,15 @@ int64_t ppca_launch_count(const ppca_ctx* ctx);
 /* ---------------------------------------------------------------- hot path */
 
 /* Writes this rank's shard of the seeded synthetic X (centred by the fp64 mean over all
- * n_global rows, rounded to spec->dtype) into the caller's device buffer X [n_local][ld].
+ * n_global rows, rounded to spec->dtype; PPCA_F32_SPLIT = the fp32 values in split layout) into the
+ * caller's device buffer X [n_local][ld].
  * n_local_out: rows written; col_mean_host: optional host double[d] receiving the mean. */
 ppca_status ppca_generate(ppca_ctx* ctx, const ppca_gen_spec* spec, void* X, int64_t ld,
                           int64_t* n_local_out, double* col_mean_host);
+
+/* In-place conversion of an fp32 shard [n_local][ld] (ld ≥ d, ld % 4 == 0, d % 8 == 0) into the
+ * PPCA_F32_SPLIT layout (same buffer, same ld).  Bit-exact: hi = RN_bf16(x), lo = RN_bf16(x − hi). */
+ppca_status ppca_split_f32(ppca_ctx* ctx, void* X, int64_t n_local, int64_t d, int64_t ld);
 
 /* Block power priming (§2.1, multi-component by re-orthonormalisation L63):
  * per iteration Y = X·Wᵀ, Z = YᵀX (fused streaming pass over X), all-reduce, W ← orth(Z)

@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libppca.so")
 
-PPCA_F32, PPCA_BF16 = 0, 1
+PPCA_F32, PPCA_BF16, PPCA_F32_SPLIT = 0, 1, 2
 PPCA_LAYOUT_CONTIGUOUS, PPCA_LAYOUT_INTERLEAVED = 0, 1
 PPCA_PLANTED_QR, PPCA_PLANTED_HOUSEHOLDER, PPCA_IMAGE_FACTOR = 0, 1, 2
 PPCA_SPECTRUM_EXP, PPCA_SPECTRUM_POWER = 0, 1
@@ -30,7 +30,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl"]
+           "ppca_last_pass_impl", "ppca_split_f32"]
 
 
 class PPCAError(RuntimeError):
@@ -89,6 +89,7 @@ def load(path: str = LIB_PATH):
         "ppca_set_timing": (I, [P, I]),
         "ppca_last_pass_impl": (I, [P]),
         "ppca_get_pass_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
+        "ppca_split_f32": (I, [P, P, I64, I64, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -128,13 +129,14 @@ def _check(ctx, status: int, what: str):
 
 
 def matrix(X, n_global: int | None = None, layout: int = PPCA_LAYOUT_CONTIGUOUS, block_rows: int = 0,
-           d: int | None = None) -> ppca_matrix:
-    """ppca_matrix for a 2-D CUDA tensor X [n_local][ld] (row-major; columns ≥ d are padding)."""
+           d: int | None = None, split: bool = False) -> ppca_matrix:
+    """ppca_matrix for a 2-D CUDA tensor X [n_local][ld] (row-major; columns ≥ d are padding).
+    split=True: a float32-sized tensor whose rows hold the PPCA_F32_SPLIT layout (ppca_split_f32)."""
     import torch
     if X.dim() != 2 or X.stride(1) != 1:
         raise ValueError("X must be a row-major 2-D tensor")
     if X.dtype == torch.float32:
-        dt = PPCA_F32
+        dt = PPCA_F32_SPLIT if split else PPCA_F32
     elif X.dtype == torch.bfloat16:
         dt = PPCA_BF16
     else:
@@ -147,13 +149,15 @@ def matrix(X, n_global: int | None = None, layout: int = PPCA_LAYOUT_CONTIGUOUS,
     return mat
 
 
-def gen_spec(spec, layout: int = PPCA_LAYOUT_CONTIGUOUS, block_rows: int = 0) -> ppca_gen_spec:
-    """ppca_gen_spec from an inputs.generate.GenSpec-like object."""
+def gen_spec(spec, layout: int = PPCA_LAYOUT_CONTIGUOUS, block_rows: int = 0, split: bool = False) -> ppca_gen_spec:
+    """ppca_gen_spec from an inputs.generate.GenSpec-like object (split=True: fp32 data written in the
+    PPCA_F32_SPLIT layout)."""
     fam = {"planted_qr": PPCA_PLANTED_QR, "planted_householder": PPCA_PLANTED_HOUSEHOLDER,
            "image_factor": PPCA_IMAGE_FACTOR}[spec.family]
     return ppca_gen_spec(fam, PPCA_SPECTRUM_EXP if spec.spectrum == "exp" else PPCA_SPECTRUM_POWER, spec.a,
                          spec.noise, int(spec.relu), spec.house_r, spec.rank,
-                         PPCA_F32 if spec.dtype == "f32" else PPCA_BF16, spec.n, spec.d, spec.seed, layout, block_rows)
+                         (PPCA_F32_SPLIT if split else PPCA_F32) if spec.dtype == "f32" else PPCA_BF16, spec.n, spec.d,
+                         spec.seed, layout, block_rows)
 
 
 # ----------------------------------------------------------------------------- multi-GPU plumbing
@@ -247,6 +251,14 @@ def ppca_generate(ctx, spec: ppca_gen_spec, X) -> tuple[int, np.ndarray]:
     _check(ctx, load().ppca_generate(ctx, ctypes.byref(spec), int(X.data_ptr()), X.stride(0), ctypes.byref(n_local),
                                      _np_ptr(mean)), "ppca_generate")
     return n_local.value, mean
+
+
+def ppca_split_f32(ctx, X, d: int | None = None) -> None:
+    """Convert the float32 CUDA tensor X [n_local][ld] in place to the PPCA_F32_SPLIT layout."""
+    if X.dim() != 2 or X.stride(1) != 1:
+        raise ValueError("X must be a row-major 2-D tensor")
+    _check(ctx, load().ppca_split_f32(ctx, int(X.data_ptr()), X.shape[0], d if d is not None else X.shape[1],
+                                      X.stride(0)), "ppca_split_f32")
 
 
 def ppca_prime_power(ctx, X: ppca_matrix, m: int, iters: int, init_seed: int, W, theta_hist: bool = False):

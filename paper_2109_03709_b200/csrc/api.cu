@@ -18,6 +18,7 @@ namespace ppca {
 
 ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_t* n_local_out, double* mu_host);
 ppca_status philox_words(Ctx* c, uint64_t seed, uint32_t stream, uint64_t first, int64_t count, uint32_t* out);
+ppca_status split_f32(Ctx* c, void* X, int64_t n_local, int64_t d, int64_t ld);
 ppca_status debug_wait_counters(unsigned long long* out16);
 
 // ----------------------------------------------------------------------------- NCCL (dlopen)
@@ -119,7 +120,10 @@ static ppca_status check_matrix(Ctx* c, const ppca_matrix* X, int m) {
   if (X->d < 1 || X->ld < X->d || X->n_local < 0 || X->n_global < X->n_local)
     return set_error(c, PPCA_ERR_DIM_MISMATCH, "bad matrix dims n_local=%lld d=%lld ld=%lld", (long long)X->n_local,
                      (long long)X->d, (long long)X->ld);
-  if (X->dtype != PPCA_F32 && X->dtype != PPCA_BF16) return set_error(c, PPCA_ERR_INVALID_ARG, "bad dtype");
+  if (X->dtype != PPCA_F32 && X->dtype != PPCA_BF16 && X->dtype != PPCA_F32_SPLIT)
+    return set_error(c, PPCA_ERR_INVALID_ARG, "bad dtype");
+  if (X->dtype == PPCA_F32_SPLIT && (X->d % 8 || (reinterpret_cast<uintptr_t>(X->data) % 16)))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "PPCA_F32_SPLIT needs d %% 8 == 0 and a 16-byte aligned X");
   if ((X->ld * (int64_t)elt_size(X->dtype)) % 16) return set_error(c, PPCA_ERR_INVALID_ARG, "ld*elt %% 16 != 0");
   if (m < 1) return set_error(c, PPCA_ERR_INVALID_ARG, "m must be >= 1");
   if (m > PPCA_MAX_M || m > X->d)
@@ -272,6 +276,14 @@ ppca_status ppca_generate(ppca_ctx* h, const ppca_gen_spec* spec, void* X, int64
   cudaSetDevice(c->device);
   PPCA_TRY(generate(c, spec, X, ld, n_local_out, col_mean_host));
   return finish(c, "ppca_generate");
+}
+
+ppca_status ppca_split_f32(ppca_ctx* h, void* X, int64_t n_local, int64_t d, int64_t ld) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(split_f32(c, X, n_local, d, ld));
+  return finish(c, "ppca_split_f32");
 }
 
 ppca_status ppca_philox_words(ppca_ctx* h, uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
@@ -505,6 +517,9 @@ ppca_status ppca_gram(ppca_ctx* h, const ppca_matrix* X, double* G) {
   if (X->dtype == PPCA_F32)
     PPCA_TRY((launch_tn_splitk<float, float>(c, (const float*)X->data, X->ld, (const float*)X->data, X->ld, P, d, d,
                                              X->n_local, ns)));
+  else if (X->dtype == PPCA_F32_SPLIT)
+    PPCA_TRY((launch_tn_splitk<SplitF32, SplitF32>(c, (const SplitF32*)X->data, X->ld, (const SplitF32*)X->data,
+                                                   X->ld, P, d, d, X->n_local, ns)));
   else
     PPCA_TRY((launch_tn_splitk<__nv_bfloat16, __nv_bfloat16>(c, (const __nv_bfloat16*)X->data, X->ld,
                                                              (const __nv_bfloat16*)X->data, X->ld, P, d, d,

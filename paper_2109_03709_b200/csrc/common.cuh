@@ -90,9 +90,24 @@ ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64);
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline size_t elt_size(ppca_dtype t) { return t == PPCA_BF16 ? 2 : 4; }
 
+// One logical element of a PPCA_F32_SPLIT row (4 bytes: pointer arithmetic p + r·ld lands on row r);
+// the row holds d bf16 hi values then d bf16 lo values, x = hi + lo (exact in fp32).
+struct SplitF32 {
+  uint32_t raw;
+};
+
 // ----------------------------------------------------------------------------- element loads
 __device__ __forceinline__ float load_elt(const float* p, int64_t i) { return p[i]; }
 __device__ __forceinline__ float load_elt(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+// element (r, c) of a matrix whose rows hold `ncols` logical columns (ncols matters for SplitF32 only)
+__device__ __forceinline__ float load_rc(const float* p, int64_t ld, int64_t r, int64_t c, int64_t) { return p[r * ld + c]; }
+__device__ __forceinline__ float load_rc(const __nv_bfloat16* p, int64_t ld, int64_t r, int64_t c, int64_t) {
+  return __bfloat162float(p[r * ld + c]);
+}
+__device__ __forceinline__ float load_rc(const SplitF32* p, int64_t ld, int64_t r, int64_t c, int64_t ncols) {
+  const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(p + r * ld);
+  return __bfloat162float(row[c]) + __bfloat162float(row[ncols + c]);
+}
 
 // ----------------------------------------------------------------------------- Philox4x32-10
 // Salmon et al. (SC'11); identical to curand_Philox4x32_10.  Counter convention:

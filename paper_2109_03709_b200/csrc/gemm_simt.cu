@@ -39,6 +39,27 @@ __device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* __rest
   }
 }
 
+template <>
+__device__ __forceinline__ void load8<SplitF32>(const SplitF32* __restrict__ p, int64_t ld, int64_t r, int64_t R,
+                                                int64_t k0, int64_t K, bool vec, float v[8]) {
+  // K = d (logical columns): the lo plane of the row starts K bf16 after the hi plane
+  const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(p + (r < R ? r : 0) * ld);
+  if (r < R && vec && k0 + 8 <= K) {
+    uint4 h = __ldg(reinterpret_cast<const uint4*>(row + k0));
+    uint4 l = __ldg(reinterpret_cast<const uint4*>(row + K + k0));
+    const uint32_t wh[4] = {h.x, h.y, h.z, h.w}, wl[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(wh[i] << 16) + __uint_as_float(wl[i] << 16);
+      v[2 * i + 1] = __uint_as_float(wh[i] & 0xffff0000u) + __uint_as_float(wl[i] & 0xffff0000u);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (r < R && k0 + i < K) ? __bfloat162float(row[k0 + i]) + __bfloat162float(row[K + k0 + i]) : 0.f;
+  }
+}
+
 // ------------------------------------------------------------------------------------ NT
 // Tile 128 (M) × 64 (N) × 16 (K); 256 threads, 8×4 outputs each.
 constexpr int NT_BM = 128, NT_BN = 64, NT_BK = 16;
@@ -119,6 +140,8 @@ template ppca_status launch_nt<float>(Ctx*, const float*, int64_t, const float*,
                                       int64_t, int64_t, int64_t, int64_t);
 template ppca_status launch_nt<__nv_bfloat16>(Ctx*, const __nv_bfloat16*, int64_t, const float*,
                                               int64_t, float*, int64_t, int64_t, int64_t, int64_t);
+template ppca_status launch_nt<SplitF32>(Ctx*, const SplitF32*, int64_t, const float*, int64_t, float*, int64_t,
+                                         int64_t, int64_t, int64_t);
 
 // ------------------------------------------------------------------------------------ TN split-K
 // Tile 64 (M) × 128 (N) × 16 (K rows); 256 threads, 4×8 outputs each; fp32 per slab → fp64.
@@ -153,7 +176,7 @@ __global__ void __launch_bounds__(256) tn_kernel(const TA* __restrict__ A, int64
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int64_t col = m0 + lc * 4 + i;
-        va[i] = (r < kend && col < M) ? load_elt(A, r * lda + col) : 0.f;
+        va[i] = (r < kend && col < M) ? load_rc(A, lda, r, col, M) : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) As[lr][lc * 4 + i] = va[i];
@@ -232,6 +255,10 @@ template ppca_status launch_tn_splitk<__nv_bfloat16, __nv_bfloat16>(Ctx*, const 
 template ppca_status launch_tn_splitk<float, __nv_bfloat16>(Ctx*, const float*, int64_t,
                                                             const __nv_bfloat16*, int64_t, double*,
                                                             int64_t, int64_t, int64_t, int);
+template ppca_status launch_tn_splitk<SplitF32, SplitF32>(Ctx*, const SplitF32*, int64_t, const SplitF32*, int64_t,
+                                                          double*, int64_t, int64_t, int64_t, int);
+template ppca_status launch_tn_splitk<float, SplitF32>(Ctx*, const float*, int64_t, const SplitF32*, int64_t,
+                                                       double*, int64_t, int64_t, int64_t, int);
 
 // ------------------------------------------------------------------------------------ reductions
 __global__ void reduce_splits_f32_kernel(const double* __restrict__ P, int nsplit, int64_t count,

@@ -441,6 +441,8 @@ static ppca_status generate_t(Ctx* c, const ppca_gen_spec* s, T* X, int64_t ld, 
   return PPCA_OK;
 }
 
+ppca_status split_f32(Ctx* c, void* X, int64_t n_local, int64_t d, int64_t ld);
+
 ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_t* n_local_out, double* mu_host) {
   if (!s || !X) return set_error(c, PPCA_ERR_INVALID_ARG, "null spec or X");
   if (s->d < 1 || s->n_global < 1 || ld < s->d) return set_error(c, PPCA_ERR_INVALID_ARG, "bad n/d/ld");
@@ -454,13 +456,57 @@ ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_
   RowMap rm{(int)s->layout, s->n_global, s->block_rows, row0, c->rank, c->world};
   double* mu = (double*)scratch(c, S_GEN3, (size_t)s->d * sizeof(double));
   if (!mu) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (s->dtype == PPCA_F32_SPLIT && s->d % 8) return set_error(c, PPCA_ERR_INVALID_ARG, "PPCA_F32_SPLIT needs d %% 8 == 0");
   ppca_status st = s->dtype == PPCA_BF16 ? generate_t<__nv_bfloat16>(c, s, (__nv_bfloat16*)X, ld, n_local, rm, mu)
                                          : generate_t<float>(c, s, (float*)X, ld, n_local, rm, mu);
   if (st != PPCA_OK) return st;
+  if (s->dtype == PPCA_F32_SPLIT) PPCA_TRY(split_f32(c, X, n_local, s->d, ld));
   if (mu_host)
     PPCA_TRY(check_cuda(c, cudaMemcpyAsync(mu_host, mu, s->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
                         "copy mean"));
   if (n_local_out) *n_local_out = n_local;
+  return PPCA_OK;
+}
+
+// ----------------------------------------------------------------------------- fp32 → split layout
+// Rows are staged through a scratch copy (the split row overwrites its own fp32 bytes), block of rows
+// at a time; hi = RN_bf16(x), lo = RN_bf16(x − hi).
+__global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t d, int64_t ld,
+                                  __nv_bfloat16* __restrict__ dst) {
+  const int64_t r = blockIdx.y;
+  if (r >= rows) return;
+  const float* s = src + r * ld;
+  __nv_bfloat16* o = dst + r * ld * 2;      // row stride in bf16 = 2·ld
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.x * blockDim.x) {
+    const float x = s[j];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    o[j] = hi;
+    o[d + j] = __float2bfloat16_rn(x - __bfloat162float(hi));
+  }
+}
+
+ppca_status split_f32(Ctx* c, void* X, int64_t n_local, int64_t d, int64_t ld) {
+  if (n_local < 0 || d < 1 || ld < d || (ld % 4) || (d % 8) || (n_local > 0 && !X) ||
+      (reinterpret_cast<uintptr_t>(X) % 16))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "ppca_split_f32: need ld >= d, ld %% 4 == 0, d %% 8 == 0, aligned X");
+  if (n_local == 0) return PPCA_OK;
+  const int64_t row_bytes = ld * 4;
+  const int64_t blk = std::max<int64_t>(1, std::min<int64_t>(n_local, ((int64_t)64 << 20) / row_bytes));
+  float* tmp = (float*)scratch(c, S_GEN2, (size_t)blk * row_bytes);
+  if (!tmp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  for (int64_t r0 = 0; r0 < n_local; r0 += blk) {
+    const int64_t rows = std::min(blk, n_local - r0);
+    uint8_t* base = (uint8_t*)X + r0 * row_bytes;
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(tmp, base, (size_t)rows * row_bytes, cudaMemcpyDeviceToDevice, c->stream),
+                        "split stage"));
+    for (int64_t y0 = 0; y0 < rows; y0 += 65535) {
+      const int64_t ry = std::min<int64_t>(65535, rows - y0);
+      dim3 grid((unsigned)std::min<int64_t>(ceil_div(d, 256), 64), (unsigned)ry);
+      split_rows_kernel<<<grid, 256, 0, c->stream>>>(tmp + y0 * ld, ry, d, ld,
+                                                    reinterpret_cast<__nv_bfloat16*>(base + y0 * row_bytes));
+      PPCA_LAUNCH_CHECK(c, "split_rows_kernel");
+    }
+  }
   return PPCA_OK;
 }
 

@@ -8,6 +8,8 @@ namespace ppca {
 ppca_status xw(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* W, int m, float* Y) {
   if (X->dtype == PPCA_F32)
     return launch_nt<float>(c, (const float*)X->data + r0 * X->ld, X->ld, W, X->d, Y, m, rows, m, X->d);
+  if (X->dtype == PPCA_F32_SPLIT)
+    return launch_nt<SplitF32>(c, (const SplitF32*)X->data + r0 * X->ld, X->ld, W, X->d, Y, m, rows, m, X->d);
   return launch_nt<__nv_bfloat16>(c, (const __nv_bfloat16*)X->data + r0 * X->ld, X->ld, W, X->d, Y, m, rows, m, X->d);
 }
 
@@ -18,6 +20,9 @@ ppca_status ytx(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const fl
   if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   if (X->dtype == PPCA_F32)
     PPCA_TRY((launch_tn_splitk<float, float>(c, Y, m, (const float*)X->data + r0 * X->ld, X->ld, P, m, X->d, rows, ns)));
+  else if (X->dtype == PPCA_F32_SPLIT)
+    PPCA_TRY((launch_tn_splitk<float, SplitF32>(c, Y, m, (const SplitF32*)X->data + r0 * X->ld, X->ld, P, m, X->d,
+                                               rows, ns)));
   else
     PPCA_TRY((launch_tn_splitk<float, __nv_bfloat16>(c, Y, m, (const __nv_bfloat16*)X->data + r0 * X->ld, X->ld, P, m,
                                                     X->d, rows, ns)));

@@ -161,12 +161,13 @@ static int pad16(int m) { return (m + 15) & ~15; }
 // iterate) may be resident, otherwise the CTA queued behind it delays the whole persistent pass
 static int persistent_ctas(const Ctx* c) { return c->side_busy ? c->sm_count - 1 : c->sm_count; }
 
-template <int MP, bool XBF16>
-static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const KAParams& kp, int grid) {
-  const size_t smem = ka::smem_bytes(MP, XBF16);
-  auto kern = xw_tc_kernel<MP, XBF16>;
+template <int MP, int XM>
+static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
+                             const KAParams& kp, int grid) {
+  const size_t smem = ka::smem_bytes(MP, XM);
+  auto kern = xw_tc_kernel<MP, XM>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, ka::NTHREADS, smem, c->stream>>>(tmW, tmX, kp);
+  kern<<<grid, ka::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, kp);
   PPCA_LAUNCH_CHECK(c, "xw_tc_kernel");
   return PPCA_OK;
 }
@@ -181,18 +182,18 @@ static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap&
   return PPCA_OK;
 }
 
-template <bool XBF16>
-static ppca_status dispatch_ka(Ctx* c, int mp, const CUtensorMap& tmW, const CUtensorMap& tmX, const KAParams& kp,
-                               int grid) {
+template <int XM>
+static ppca_status dispatch_ka(Ctx* c, int mp, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                               const CUtensorMap& tmXlo, const KAParams& kp, int grid) {
   switch (mp) {
-    case 16: return launch_ka<16, XBF16>(c, tmW, tmX, kp, grid);
-    case 32: return launch_ka<32, XBF16>(c, tmW, tmX, kp, grid);
-    case 48: return launch_ka<48, XBF16>(c, tmW, tmX, kp, grid);
-    case 64: return launch_ka<64, XBF16>(c, tmW, tmX, kp, grid);
-    case 80: return launch_ka<80, XBF16>(c, tmW, tmX, kp, grid);
-    case 96: return launch_ka<96, XBF16>(c, tmW, tmX, kp, grid);
-    case 112: return launch_ka<112, XBF16>(c, tmW, tmX, kp, grid);
-    case 128: return launch_ka<128, XBF16>(c, tmW, tmX, kp, grid);
+    case 16: return launch_ka<16, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 32: return launch_ka<32, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 48: return launch_ka<48, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 64: return launch_ka<64, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 80: return launch_ka<80, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 96: return launch_ka<96, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 112: return launch_ka<112, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 128: return launch_ka<128, XM>(c, tmW, tmX, tmXlo, kp, grid);
   }
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
@@ -218,10 +219,18 @@ ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan)
   if (X->d % 8 != 0 || X->d < 64) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs d %% 8 == 0, d >= 64");
   if (m > 128 || m < 1) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs m <= 128");
   if (X->n_local < 128) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs >= 128 local rows");
-  if (X->dtype == PPCA_BF16 && (reinterpret_cast<uintptr_t>(X->data) % 16)) return set_error(c, PPCA_ERR_UNSUPPORTED, "X not 16B aligned");
-  if (X->dtype == PPCA_F32 && (reinterpret_cast<uintptr_t>(X->data) % 16)) return set_error(c, PPCA_ERR_UNSUPPORTED, "X not 16B aligned");
+  if (reinterpret_cast<uintptr_t>(X->data) % 16) return set_error(c, PPCA_ERR_UNSUPPORTED, "X not 16B aligned");
   plan->impl = 2;
   return PPCA_OK;
+}
+
+// TMA maps of X's bf16 planes (box 64 columns × box_rows rows): bf16 X → tmX; split → tmX = hi plane,
+// tmXlo = lo plane (the row stride of a split row is 4·ld bytes = 2·ld bf16)
+static bool make_x_maps(const ppca_matrix* X, uint32_t box_rows, CUtensorMap* hi, CUtensorMap* lo) {
+  if (X->dtype == PPCA_BF16) return make_map_bf16(hi, X->data, X->d, X->n_local, X->ld, box_rows);
+  const __nv_bfloat16* base = static_cast<const __nv_bfloat16*>(X->data);
+  return make_map_bf16(hi, base, X->d, X->n_local, 2 * X->ld, box_rows) &&
+         make_map_bf16(lo, base + X->d, X->d, X->n_local, 2 * X->ld, box_rows);
 }
 
 // W' (bf16 + its fp32 value copy) → S_TC1;  returns pointers
@@ -237,13 +246,10 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
 
 static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, int mp, double* S,
                           __nv_bfloat16* YT, int64_t ldyt) {
-  CUtensorMap tmW, tmX;
+  CUtensorMap tmW, tmX, tmXlo;
   if (!make_map_bf16(&tmW, Wb, X->d, 2 * mp, X->d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
-  if (X->dtype == PPCA_BF16) {
-    if (!make_map_bf16(&tmX, X->data, X->d, X->n_local, X->ld, 128)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
-  } else {
-    tmX = tmW;   // unused
-  }
+  tmX = tmXlo = tmW;   // unused unless X is staged by TMA
+  if (X->dtype != PPCA_F32 && !make_x_maps(X, 128, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   KAParams kp;
   kp.X = X->data; kp.n = X->n_local; kp.d = X->d; kp.ld = X->ld; kp.m = m; kp.mp = mp;
   kp.ntiles = ceil_div(X->n_local, ka::BM);
@@ -256,7 +262,9 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * mp * mp * sizeof(double));
   if (!Spart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   kp.Spart = Spart;
-  PPCA_TRY(X->dtype == PPCA_BF16 ? dispatch_ka<true>(c, mp, tmW, tmX, kp, grid) : dispatch_ka<false>(c, mp, tmW, tmX, kp, grid));
+  PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
+           : X->dtype == PPCA_F32_SPLIT ? dispatch_ka<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
+                                        : dispatch_ka<0>(c, mp, tmW, tmX, tmXlo, kp, grid));
   reduce_spart_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
   return PPCA_OK;
@@ -298,15 +306,13 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   float* Zp = (float*)scratch(c, S_PART, (size_t)bp.nrg * dpad * mp * sizeof(float));
   if (!Zp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   bp.Zp = Zp;
-  CUtensorMap tmYT, tmX;
+  CUtensorMap tmYT, tmX, tmXlo;
   if (!make_map_bf16(&tmYT, YT, ldyt, 2 * mp, ldyt, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map YT failed");
-  if (X->dtype == PPCA_BF16) {
-    if (!make_map_bf16(&tmX, X->data, d, n, X->ld, kb::KR)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
-  } else {
-    tmX = tmYT;
-  }
+  tmX = tmYT;
+  // product 2 reads X_hi only: bf16 X, or the hi plane of a split X, by TMA
+  if (X->dtype != PPCA_F32 && !make_x_maps(X, kb::KR, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   const int grid = (int)std::min<int64_t>(ctas, bp.ndg * bp.nrg);
-  PPCA_TRY(X->dtype == PPCA_BF16 ? dispatch_kb<true>(c, mp, tmYT, tmX, bp, grid) : dispatch_kb<false>(c, mp, tmYT, tmX, bp, grid));
+  PPCA_TRY(X->dtype != PPCA_F32 ? dispatch_kb<true>(c, mp, tmYT, tmX, bp, grid) : dispatch_kb<false>(c, mp, tmYT, tmX, bp, grid));
   reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;

@@ -27,11 +27,12 @@ constexpr int NTHREADS = (W_CTRL + 1) * 32;
 constexpr int SFLUSH = 8;          // tiles between fp32 → fp64 flushes of the S partial
 constexpr int PF = 0;              // converter L2-prefetch distance in K chunks (measured: prefetching hurts; off)
 constexpr uint32_t XST = BM * 128; // one bf16 X stage (hi or lo)
-__host__ __device__ constexpr int nst(int MP, bool xbf16) { return xbf16 ? 4 : (MP <= 64 ? 3 : 2); }
+// XM (X mode): 0 = fp32 X converted by the converter warps, 1 = bf16 X by TMA, 2 = PPCA_F32_SPLIT by TMA
+__host__ __device__ constexpr int nst(int MP, int xm) { return xm == 1 ? 4 : (MP <= 64 ? 3 : 2); }
 __host__ __device__ constexpr int nws(int MP) { return MP <= 64 ? 4 : 2; }
 __host__ __device__ constexpr int ntb(int MP) { return 2 * MP <= 128 ? 4 : 2; }
-__host__ __device__ constexpr size_t smem_bytes(int MP, bool xbf16) {
-  return 1024 + (size_t)nst(MP, xbf16) * (xbf16 ? XST : 2 * XST) + (size_t)nws(MP) * 2 * MP * 128 +
+__host__ __device__ constexpr size_t smem_bytes(int MP, int xm) {
+  return 1024 + (size_t)nst(MP, xm) * (xm == 1 ? XST : 2 * XST) + (size_t)nws(MP) * 2 * MP * 128 +
          (size_t)BM * (MP + 4) * 4 + 512;
 }
 }  // namespace ka
@@ -47,13 +48,16 @@ struct KAParams {
   int dbg;                // experiment switches (env PPCA_DBG; 0 in production)
 };
 
-template <int MP, bool XBF16>
+template <int MP, int XM>
 __global__ void __launch_bounds__(ka::NTHREADS, 1)
-    xw_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, KAParams p) {
+    xw_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ CUtensorMap tmXlo, KAParams p) {
   using namespace ka;
-  constexpr uint32_t XSTG = XBF16 ? XST : 2 * XST;  // X stage: hi (+ lo for fp32 X)
-  constexpr int NST = nst(MP, XBF16), NWS = nws(MP), NTB = ntb(MP);
-  static_assert(smem_bytes(MP, XBF16) <= 227 * 1024, "kernel A shared memory budget");
+  constexpr bool TMAX = XM != 0;                    // X stages filled by TMA (bf16 / split planes)
+  constexpr bool LO = XM != 1;                      // an X_lo plane exists (fp32 converted, or split)
+  constexpr uint32_t XSTG = LO ? 2 * XST : XST;     // X stage: hi (+ lo)
+  constexpr int NST = nst(MP, XM), NWS = nws(MP), NTB = ntb(MP);
+  static_assert(smem_bytes(MP, XM) <= 227 * 1024, "kernel A shared memory budget");
   constexpr int NB = 2 * MP;                        // UMMA N: [W_hi; W_lo]
   constexpr uint32_t WST = NB * 128;
   constexpr uint32_t TCOLS = NTB * NB <= 32 ? 32 : (NTB * NB <= 64 ? 64 : (NTB * NB <= 128 ? 128 : (NTB * NB <= 256 ? 256 : 512)));
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
-      mbar_init(&full[s], XBF16 ? 1 : NCONV);
+      mbar_init(&full[s], TMAX ? 1 : NCONV);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < NWS; ++s) {
@@ -90,7 +94,8 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
   }
   if (warp == W_CTRL && lane == 0) {
     tma_prefetch_desc(&tmW);
-    if (XBF16) tma_prefetch_desc(&tmX);
+    if (TMAX) tma_prefetch_desc(&tmX);
+    if (XM == 2) tma_prefetch_desc(&tmXlo);
   }
   if (warp == W_CTRL) tmem_alloc<TCOLS>(tmem_slot);
   tc_fence_before();
@@ -111,16 +116,17 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
           mbar_arrive_expect_tx(&wfull[s], WST);
           tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
         }
-    } else if (XBF16 && lane == 1) {
-      // ---------------------------------------------------------------- X ring (bf16 X by TMA)
+    } else if (TMAX && lane == 1) {
+      // ---------------------------------------------------------------- X ring (bf16 X / split planes by TMA)
       const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t t = t0; t < p.ntiles; t += tstep)
         for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], XST);
+          mbar_arrive_expect_tx(&full[s], XSTG);
           tma_load_2d_hint(sX + s * XSTG, &tmX, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
+          if (XM == 2) tma_load_2d_hint(sX + s * XSTG + XST, &tmXlo, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
         }
     } else if (lane == 2) {
       // ---------------------------------------------------------------- MMA issue (one thread)
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
                 mma_bf16(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024), ID,
                          (kc != g * KSEG) || kk != 0);
                 // hi columns += X_lo·W_hiᵀ   (fp32 X only)
-                if (!XBF16 && !(p.dbg & 8))
+                if (LO && !(p.dbg & 8))
                   mma_bf16(dcol, smem_desc_sw128(xa + XST + kk * 32, 16, 1024),
                            smem_desc_sw128(wa + kk * 32, 16, 1024), ID_HI, 1);
               }
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
     }
   } else if (warp >= W_CONV0 && warp < W_CONV0 + NCONV) {
     // ------------------------------------------------------------------ fp32 → bf16 pair converters
-    if (!XBF16) {
+    if (XM == 0) {
       const float* X = reinterpret_cast<const float*>(p.X);
       const int cw = warp - W_CONV0;
       const int sub = lane >> 4, cl = lane & 15;

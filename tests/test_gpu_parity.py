@@ -82,6 +82,47 @@ def test_generate_matches_host_generator(P, ctx, name):
         assert np.mean(got != Xs) < 1e-3
 
 
+def _split_ref(x32):
+    """Host reference of the split layout: hi = RN_bf16(x), lo = RN_bf16(x − hi) (x − hi exact in fp64)."""
+    x = x32.astype(np.float64)
+    hi = G.f64_to_bf16_bits(x)
+    lo = G.f64_to_bf16_bits(x - G.bf16_bits_to_f64(hi))
+    return hi, lo
+
+
+def test_split_f32_bit_exact_and_ragged(P, ctx):
+    import torch
+    rng = np.random.default_rng(12)
+    n, d, ld = 37, 72, 80                               # ragged rows, padded stride
+    x = (rng.standard_normal((n, d)) * np.exp(rng.uniform(-20, 20, (n, d)))).astype(np.float32)
+    x[0, :4] = [0.0, -0.0, 1e-30, -3.0e38]              # zero, signed zero, tiny, large
+    Xd = torch.zeros((n, ld), dtype=torch.float32, device="cuda")
+    Xd[:, :d] = torch.from_numpy(x).cuda()
+    P.ppca_split_f32(ctx, Xd, d)
+    raw = Xd.cpu().numpy().view(np.uint16).reshape(n, 2 * ld)
+    hi, lo = _split_ref(x)
+    np.testing.assert_array_equal(raw[:, :d], hi)
+    np.testing.assert_array_equal(raw[:, d:2 * d], lo)
+    # the pair represents x to 2^-17 relative
+    rec = G.bf16_bits_to_f64(hi) + G.bf16_bits_to_f64(lo)
+    ok = np.abs(x) > 1e-30
+    assert np.max(np.abs(rec[ok] - x[ok]) / np.abs(x[ok])) <= 2.0 ** -16
+    with pytest.raises(P.PPCAError):
+        P.ppca_split_f32(ctx, torch.zeros((4, 20), device="cuda"), 20)   # d % 8 != 0
+    P.ppca_split_f32(ctx, torch.zeros((0, 16), device="cuda"), 16)      # empty shard is a no-op
+
+
+def test_generate_split_equals_split_of_generate(P, ctx):
+    import torch
+    s = C.SMALL["C3s"].spec
+    A = torch.zeros((s.n, s.d), dtype=torch.float32, device="cuda")
+    B = torch.zeros_like(A)
+    P.ppca_generate(ctx, P.gen_spec(s), A)
+    P.ppca_split_f32(ctx, A, s.d)
+    P.ppca_generate(ctx, P.gen_spec(s, split=True), B)
+    assert torch.equal(A.view(torch.int32), B.view(torch.int32))
+
+
 # ----------------------------------------------------------------------------- power priming + refine
 @pytest.fixture
 def impl(P, ctx, request):
@@ -90,22 +131,33 @@ def impl(P, ctx, request):
     P.ppca_set_pass_impl(ctx, 0)
 
 
+def _device_matrix(P, ctx, Xs, spec, split):
+    """Stored host X → device ppca_matrix; split=True converts the fp32 rows in place to the
+    PPCA_F32_SPLIT layout through the C ABI (ppca_split_f32)."""
+    Xd = U.upload(Xs, spec.dtype)
+    if split:
+        P.ppca_split_f32(ctx, Xd, spec.d)
+    return P.matrix(Xd, d=spec.d, split=split)
+
+
+@pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
 @pytest.mark.parametrize("impl", [1, 2], indirect=True, ids=["simt", "tcgen05"])
 @pytest.mark.parametrize("name", ["C1", "C3s", "C5s"])
-def test_power_priming_and_refine_parity(P, ctx, name, impl):
+def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
     import torch
     if impl == 2 and name == "C1":
         pytest.skip("auto keeps 0.5 MB shards on the fp32 SIMT pass (bf16 rounding of X at n=2000 ~1e-4)")
     w = C.SMALL[name]
     s = w.spec
+    if split and s.dtype != "f32":
+        pytest.skip("the split layout is for fp32 data")
     Xs, X64 = _host(w)
     lam, T = O.truth(X64)
     W0 = G.init_gaussians(w.init_seed, w.m, s.d)
     W_ref, S_hist = O.prime_power(X64, W0, w.iters)
     E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, W_ref, w.k)
 
-    Xd = U.upload(Xs, s.dtype)
-    Xm = P.matrix(Xd, d=s.d)
+    Xm = _device_matrix(P, ctx, Xs, s, split)
     W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
     th_hist = P.ppca_prime_power(ctx, Xm, w.m, w.iters, w.init_seed, W, theta_hist=True)
     assert P.ppca_last_pass_impl(ctx) == impl
@@ -121,12 +173,12 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl):
         err_t = U.ritz_rel_err(th_hist[t], ref)
         worst = max(worst, err_t)
         assert err_t < _tol(s), f"iteration {t}"
-    print(f"\n[parity] {name} impl={impl}: per-iteration Ritz rel err max {worst:.3e} (tol {_tol(s)})")
+    print(f"\n[parity] {name} impl={impl} split={split}: per-iteration Ritz rel err max {worst:.3e} (tol {_tol(s)})")
     E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
     th, dim = P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
     assert dim == w.m
     err = U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), name, th_all_ref)
-    print(f"[parity] {name} impl={impl}: refine Ritz rel err {err:.3e}")
+    print(f"[parity] {name} impl={impl} split={split}: refine Ritz rel err {err:.3e}")
     # Cauchy interlacing of the GPU Ritz values with the true spectrum
     d, m = s.d, w.m
     for i in range(w.k):
@@ -134,7 +186,8 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl):
 
 
 # ----------------------------------------------------------------------------- minibatch primings
-def test_oja_parity_c2s(P, ctx):
+@pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
+def test_oja_parity_c2s(P, ctx, split):
     import torch
     w = C.SMALL["C2s"]
     s = w.spec
@@ -143,8 +196,7 @@ def test_oja_parity_c2s(P, ctx):
     steps = w.steps
     W_ref, vel_ref = O.prime_oja(X64, G.init_gaussians(w.init_seed, w.m, s.d), w.batch, w.alpha, w.momentum, steps)
     E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, W_ref, w.k)
-    Xd = U.upload(Xs, s.dtype)
-    Xm = P.matrix(Xd, d=s.d)
+    Xm = _device_matrix(P, ctx, Xs, s, split)
     W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
     vel = torch.zeros_like(W)
     nxt = P.ppca_prime_oja(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, w.init_seed, W, vel, 0)
@@ -157,7 +209,8 @@ def test_oja_parity_c2s(P, ctx):
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), "C2s", th_all_ref)
 
 
-def test_eigengame_parity_c4s(P, ctx):
+@pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
+def test_eigengame_parity_c4s(P, ctx, split):
     import torch
     w = C.SMALL["C4s"]
     s = w.spec
@@ -166,8 +219,7 @@ def test_eigengame_parity_c4s(P, ctx):
     steps = w.steps
     V_ref, _ = O.prime_eigengame(X64, G.init_gaussians(w.init_seed, w.m, s.d), w.batch, w.alpha, w.momentum, steps)
     E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, V_ref, w.k)
-    Xd = U.upload(Xs, s.dtype)
-    Xm = P.matrix(Xd, d=s.d)
+    Xm = _device_matrix(P, ctx, Xs, s, split)
     V = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
     vel = torch.zeros_like(V)
     P.ppca_prime_eigengame(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, w.init_seed, V, vel, 0)
@@ -180,9 +232,10 @@ def test_eigengame_parity_c4s(P, ctx):
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), "C4s", th_all_ref)
 
 
+@pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
 @pytest.mark.parametrize("impl", [1, 2], indirect=True, ids=["simt", "tcgen05"])
 @pytest.mark.parametrize("name", ["C2s", "C4s"])
-def test_refine_parity_random_priming(P, ctx, name, impl):
+def test_refine_parity_random_priming(P, ctx, name, impl, split):
     """Refine (Alg. 1 steps 2–5) of a perturbed-truth priming on the minibatch workloads' data."""
     import torch
     w = C.SMALL[name]
@@ -193,7 +246,7 @@ def test_refine_parity_random_priming(P, ctx, name, impl):
     V = T[: w.m] + 0.05 * rng.standard_normal((w.m, s.d)) / math.sqrt(s.d)
     V32 = V.astype(np.float32)
     E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, V32.astype(np.float64), w.k)
-    Xm = P.matrix(U.upload(Xs, s.dtype), d=s.d)
+    Xm = _device_matrix(P, ctx, Xs, s, split)
     E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
     th, dim = P.ppca_refine(ctx, Xm, torch.from_numpy(V32).cuda(), w.m, w.k, E)
     assert P.ppca_last_pass_impl(ctx) == impl and dim == w.m
