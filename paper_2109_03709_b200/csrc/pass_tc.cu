@@ -126,6 +126,34 @@ __global__ void __launch_bounds__(256) reduce_spart_kernel(const double* __restr
   }
 }
 
+// ============================================================================ kernel A, TMA-staged X (tc_xw2.cuh)
+#include "tc_xw2.cuh"
+
+// S[i][j] = S[j][i] = Σ_cta (Sp[cta][a][b] + Sp[cta][a + mp][b]),  a = min(i,j), b = max(i,j)
+// (S partials of the tensor-core S: rows a and a+mp hold the hi- and lo-row halves of D; fixed order)
+__global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __restrict__ Spart, int nparts, int mp,
+                                                            int m, double* __restrict__ S) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < m * m) {
+    const int i = e / m, j = e % m;
+    const int a = min(i, j), b = max(i, j);
+    for (int c = warp; c < nparts; c += 8) {
+      const double* P = Spart + (int64_t)c * 2 * mp * mp;
+      s += P[a * mp + b] + P[(a + mp) * mp + b];
+    }
+  }
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && e < m * m) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    S[e] = t;
+  }
+}
+
 // ============================================================================ kernel B (tc_xty.cuh)
 #include "tc_xty.cuh"
 
@@ -180,6 +208,33 @@ static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap&
   kern<<<grid, kb::NTHREADS, smem, c->stream>>>(tmYT, tmX, bp);
   PPCA_LAUNCH_CHECK(c, "xty_tc_kernel");
   return PPCA_OK;
+}
+
+template <int MP, int XM>
+static ppca_status launch_ka2(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
+                              const KAParams& kp, int grid) {
+  const size_t smem = ka2::Cfg<MP, XM>::SMEM;
+  auto kern = xw_tma_kernel<MP, XM>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, ka2::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, kp);
+  PPCA_LAUNCH_CHECK(c, "xw_tma_kernel");
+  return PPCA_OK;
+}
+
+template <int XM>
+static ppca_status dispatch_ka2(Ctx* c, int mp, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                                const CUtensorMap& tmXlo, const KAParams& kp, int grid) {
+  switch (mp) {
+    case 16: return launch_ka2<16, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 32: return launch_ka2<32, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 48: return launch_ka2<48, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 64: return launch_ka2<64, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 80: return launch_ka2<80, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 96: return launch_ka2<96, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 112: return launch_ka2<112, XM>(c, tmW, tmX, tmXlo, kp, grid);
+    case 128: return launch_ka2<128, XM>(c, tmW, tmX, tmXlo, kp, grid);
+  }
+  return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
 
 template <int XM>
@@ -259,13 +314,19 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   kp.dbg = dbg;
   int grid = (int)std::min<int64_t>(persistent_ctas(c), kp.ntiles);
-  double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * mp * mp * sizeof(double));
+  // TMA-staged X (bf16, split) runs kernel A2; its S partial has 2·mp rows when S is on the tensor cores
+  const bool tma_x = X->dtype != PPCA_F32;
+  const bool smma = tma_x && mp == 64;
+  double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * (smma ? 2 : 1) * mp * mp * sizeof(double));
   if (!Spart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   kp.Spart = Spart;
-  PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
-           : X->dtype == PPCA_F32_SPLIT ? dispatch_ka<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
+  PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka2<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
+           : X->dtype == PPCA_F32_SPLIT ? dispatch_ka2<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
                                         : dispatch_ka<0>(c, mp, tmW, tmX, tmXlo, kp, grid));
-  reduce_spart_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+  if (smma)
+    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+  else
+    reduce_spart_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
   return PPCA_OK;
 }
