@@ -1,8 +1,8 @@
 // tc_xw2.cuh — kernel A for TMA-staged X (a bf16 X, or the two bf16 planes of a PPCA_F32_SPLIT X):
 //   Y_t = X_t·W'ᵀ  and  S += Y_tᵀY_t   (§8 rows a2 / a7; PAPER.md L61-63 product, L260-269 projected Gram).
 //
-// Persistent, one CTA per SM, 5 warps: 0-3 epilogue (TMEM lane quadrants, thread = tile row), 4 control
-// (lane 0: W' TMA ring, lane 1: X TMA ring, lane 2: MMA issue; the warp owns TMEM).  No CUDA-core
+// Persistent, one CTA per SM, 7 warps: 0-3 epilogue (TMEM lane quadrants, thread = tile row), 4 W' TMA
+// ring, 5 X TMA ring, 6 MMA issue (owns TMEM).  No CUDA-core
 // conversion: TMA writes the bf16 planes straight into SWIZZLE_128B atoms that the UMMA descriptors read.
 //
 // Product 1 per 128-row tile and 64-column K chunk (UMMA M=128, K=16):  [hi | lo] columns (+)= X_hi·[W_hi; W_lo]ᵀ
@@ -23,10 +23,13 @@ constexpr int BM = 128;            // rows per tile (UMMA M)
 constexpr int BK = 64;             // bf16 K elements per chunk (one 128-byte swizzle row)
 constexpr int KSEG = 16;           // chunks per accumulation segment
 constexpr int SFLUSH = 8;          // tiles between fp32 → fp64 flushes of the S partial
-constexpr int W_CTRL = 4;
-constexpr int NTHREADS = 5 * 32;
+// warps 0-3 epilogue, 4 W' producer, 5 X producer, 6 MMA issuer (separate warps: a lane spinning on an
+// mbarrier must not delay the other roles' lanes of the same warp)
+constexpr int W_WPROD = 4, W_XPROD = 5, W_MMA = 6;
+constexpr int NTHREADS = 7 * 32;
 constexpr uint32_t XST = BM * 128; // one bf16 plane stage (128 rows × 64 columns)
 constexpr uint32_t YBLK = BM * 128;   // one 64-feature block of the Y operand tile
+constexpr int XPF = 0;             // X chunks prefetched into L2 ahead of the TMA loads (measured: hurts)
 
 template <int MP, int XM>
 struct Cfg {
@@ -39,9 +42,10 @@ struct Cfg {
       TUSED <= 32 ? 32 : (TUSED <= 64 ? 64 : (TUSED <= 128 ? 128 : (TUSED <= 256 ? 256 : 512)));
   static constexpr int PLANES = XM == 2 ? 2 : 1;
   static constexpr uint32_t XSTG = PLANES * XST;
-  static constexpr int NWS = SMMA ? 3 : (MP <= 64 ? 4 : 2);
+  static constexpr int NWS = MP <= 64 ? 4 : 2;
   static constexpr uint32_t WST = NB * 128;
-  static constexpr size_t YS = (size_t)BM * (MP + 4) * 4;       // fp32 Y rows (segment sums, CUDA-core S)
+  // fp32 Y rows for the CUDA-core S (the tensor-core S keeps the segment sums in registers)
+  static constexpr size_t YS = SMMA ? 0 : (size_t)BM * (MP + 4) * 4;
   static constexpr size_t YSM = SMMA ? (size_t)2 * YBLK : 0;    // bf16 [Y_hi | Y_lo] operand tile
   static constexpr size_t FIXED = 1024 + (size_t)NWS * WST + YSM + YS + 512;
   static constexpr int NST_FIT = (int)((227 * 1024 - FIXED) / XSTG);
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   uint8_t* sW = sX + NST * XSTG;                     // NWS × WST
   uint8_t* sY = sW + NWS * WST;                      // YSM: [Y_hi block | Y_lo block]
   float* Ys = reinterpret_cast<float*>(sY + CF::YSM);   // BM × YS_LD
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Ys + BM * YS_LD);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(Ys) + CF::YS);
   uint64_t* full = bars;
   uint64_t* empty = full + NST;
   uint64_t* wfull = empty + NST;
@@ -98,12 +102,12 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
     mbar_init(sfull, 1);
     fence_barrier_init();
   }
-  if (warp == W_CTRL && lane == 0) {
+  if (warp == W_XPROD && lane == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
     if (LO) tma_prefetch_desc(&tmXlo);
   }
-  if (warp == W_CTRL) tmem_alloc<TCOLS>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc<TCOLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -111,31 +115,42 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   const int64_t t0 = blockIdx.x, tstep = gridDim.x;
   const int64_t nseg = (p.nk + KSEG - 1) / KSEG;
 
-  if (warp == W_CTRL) {
-    if (lane == 0) {
+  if (warp >= W_WPROD) {
+    if (warp == W_WPROD && lane == 0) {
       // ---------------------------------------------------------------- W' ring (TMA, L2-resident)
       uint32_t it = 0;
-      for (int64_t t = t0; t < p.ntiles; t += tstep)
+      for (int64_t t = t0; t < p.ntiles && !(p.dbg & 32); t += tstep)
         for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
           const uint32_t s = it % NWS, ph = (it / NWS) & 1;
           mbar_wait(&wempty[s], ph ^ 1);
           mbar_arrive_expect_tx(&wfull[s], WST);
           tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
         }
-    } else if (lane == 1) {
+    } else if (warp == W_XPROD && lane == 0) {
       // ---------------------------------------------------------------- X ring (hi [+ lo] planes)
       const uint64_t pol = policy_evict_first();
+      // L2 prefetch cursor PFD chunks ahead of the loads (PPCA_DBG bit 128 disables it)
+      const int PFD = (p.dbg & 128) ? 0 : XPF;
+      int64_t pt = t0, pk = 0;
+      auto prefetch = [&]() {
+        if (pt >= p.ntiles) return;
+        tma_prefetch_2d(&tmX, (int32_t)(pk * BK), (int32_t)(pt * BM));
+        if (LO) tma_prefetch_2d(&tmXlo, (int32_t)(pk * BK), (int32_t)(pt * BM));
+        if (++pk == p.nk) { pk = 0; pt += tstep; }
+      };
+      for (int i = 0; i < PFD; ++i) prefetch();
       uint32_t it = 0;
       for (int64_t t = t0; t < p.ntiles; t += tstep)
         for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
+          if (PFD) prefetch();
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], XSTG);
+          mbar_arrive_expect_tx(&full[s], (p.dbg & 64) ? XST : XSTG);
           tma_load_2d_hint(sX + s * XSTG, &tmX, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
-          if (LO)
+          if (LO && !(p.dbg & 64))
             tma_load_2d_hint(sX + s * XSTG + XST, &tmXlo, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
         }
-    } else if (lane == 2) {
+    } else if (warp == W_MMA && lane == 0) {
       // ---------------------------------------------------------------- MMA issue (one thread)
       constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, BM, NB, 0, 0);
       constexpr uint32_t ID_HI = idesc(FMT_BF16, FMT_BF16, BM, MP, 0, 0);
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk) {
           const uint64_t dy = smem_desc_sw128(ya + kk * 2048, YBLK, 1024);
-          mma_bf16(tmem + CF::SCOL0, dy, dy, ID_S, kk != 0);
+          if (!(p.dbg & 2)) mma_bf16(tmem + CF::SCOL0, dy, dy, ID_S, kk != 0);
         }
         mma_commit(sfull);
       };
@@ -162,12 +177,12 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           for (int64_t kc = g * KSEG; kc < k1; ++kc, ++it) {
             const uint32_t s = it % NST, ph = (it / NST) & 1;
             const uint32_t ws = it % NWS, wph = (it / NWS) & 1;
-            mbar_wait(&wfull[ws], wph);
+            if (!(p.dbg & 32)) mbar_wait(&wfull[ws], wph);
             mbar_wait(&full[s], ph);
             tc_fence_after();
             const uint32_t xa = smem_u32(sX + s * XSTG), wa = smem_u32(sW + ws * WST);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
+            for (int kk = 0; kk < BK / 16 && !(p.dbg & 1); ++kk) {
               mma_bf16(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024), ID,
                        (kc != g * KSEG) || kk != 0);
               if (LO)
@@ -228,17 +243,13 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           const uint32_t b = sg % NTB, tph = (sg / NTB) & 1;
           mbar_wait(&tfull[b], tph);
           tc_fence_after();
-          const bool last = g == nseg - 1;
 #pragma unroll
           for (int c0 = 0; c0 < MP; c0 += 8) {
             float v[8], w[8];
             tmem_ld8(tmem + tl + b * NB + c0, v);        // X'·W_hiᵀ
             tmem_ld8(tmem + tl + b * NB + MP + c0, w);   // X'·W_loᵀ
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float cur = (g == 0 ? 0.f : yrow[c0 + j]) + (v[j] + w[j]);
-              if (last) y[c0 + j] = cur; else yrow[c0 + j] = cur;
-            }
+            for (int j = 0; j < 8; ++j) y[c0 + j] = (g == 0 ? 0.f : y[c0 + j]) + (v[j] + w[j]);
           }
           tc_fence_before();
           __syncwarp();
@@ -348,5 +359,5 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == W_CTRL) tmem_dealloc<TCOLS>(tmem);
+  if (warp == W_MMA) tmem_dealloc<TCOLS>(tmem);
 }
