@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__
 ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G) {
   int tiles = (int)ceil_div(m, 32);
   int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
-  int64_t maxs = ceil_div(d, 256);
+  int64_t maxs = ceil_div(d, 64);
   int nsplit = (int)std::max<int64_t>(1, std::min(want, maxs));
   int64_t cps = ceil_div(ceil_div(d, nsplit), 64) * 64;
   nsplit = (int)ceil_div(d, cps);
@@ -60,58 +60,60 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < m; i += nt) diag0[i] = A[i * m + i];
   __syncthreads();
-  __shared__ double piv;
-  __shared__ int dropped;
-  __shared__ double colj[PPCA_MAX_M];    // column j of L (row-contiguous copy: no 32-way bank conflicts)
+  __shared__ double colj[PPCA_MAX_M];    // scaled column j of L (row-contiguous copy)
   for (int j = 0; j < m; ++j) {
+    // phase 1: every thread derives the pivot decision from A[j][j] (no broadcast barrier needed)
+    const double p = A[j * m + j];
+    const bool dr = drop > 0.0 ? !(p > drop * drop * diag0[j]) : (!(p > 0.0) || !isfinite(p));
     if (tid == 0) {
-      double p = A[j * m + j];
-      int dr = 0;
-      if (drop > 0.0) {
-        dr = !(p > drop * drop * diag0[j]);
-      } else if (!(p > 0.0) || !isfinite(p)) {
-        atomicOr(d_err, DEV_COLLAPSE);
-        dr = 1;
-      }
-      dropped = dr;
       keep[j] = !dr;
-      piv = dr ? 0.0 : sqrt(p);
+      if (dr && drop <= 0.0) atomicOr(d_err, DEV_COLLAPSE);
+    }
+    if (dr) {
+      for (int i = j + tid; i < m; i += nt) colj[i] = 0.0;
+    } else {
+      const double piv = sqrt(p), rp = 1.0 / piv;
+      for (int i = j + tid; i < m; i += nt) colj[i] = (i == j) ? piv : A[i * m + j] * rp;
     }
     __syncthreads();
-    if (dropped) {
-      for (int i = j + tid; i < m; i += nt) A[i * m + j] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    for (int i = j + tid; i < m; i += nt) {
-      const double v = (i == j) ? piv : A[i * m + j] / piv;
-      A[i * m + j] = v;
-      colj[i] = v;
-    }
-    __syncthreads();
-    const int rem = m - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k <= i) A[i * m + k] -= colj[i] * colj[k];
+    // phase 2: write column j, update the trailing lower triangle A[i][k] -= l_i l_k (k ≤ i)
+    for (int i = j + tid; i < m; i += nt) A[i * m + j] = colj[i];
+    if (!dr) {
+      const int rem = m - j - 1;
+      for (int e = tid; e < rem * rem; e += nt) {
+        const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+        if (k <= i) A[i * m + k] -= colj[i] * colj[k];
+      }
     }
     __syncthreads();
   }
 }
 
-// Forward substitution: Linv (global, row-major m×m), thread per column.
+// Linv = L⁻¹ (rows of dropped pivots zero), rows in order; for each row all columns cc ≤ i at once, with
+// blockDim/m threads per column splitting Σ_{cc≤j<i} L[i][j]·Linv[j][cc] (reduced in fixed order).
 __device__ void block_lower_inverse(const double* L, int m, const int* keep, double* Linv) {
-  for (int cc = threadIdx.x; cc < m; cc += blockDim.x) {
-    for (int i = 0; i < m; ++i) {
+  __shared__ double red[512];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int gpc = max(1, min(nt, 512) / m);
+  const int cc = tid % m, q = tid / m;
+  for (int i = 0; i < m; ++i) {
+    double part = 0.0;
+    if (q < gpc && cc < i && keep[i])
+      for (int j = cc + q; j < i; j += gpc) part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
+    if (q < gpc) red[q * m + cc] = part;
+    __syncthreads();
+    for (int c2 = tid; c2 < m; c2 += nt) {
       double v = 0.0;
-      if (i >= cc && keep[i]) {
-        double s = (i == cc) ? 1.0 : 0.0;
-        for (int j = cc; j < i; ++j) s -= L[i * m + j] * Linv[(int64_t)j * m + cc];
-        v = s / L[i * m + i];
+      if (keep[i] && c2 <= i) {
+        double sum = 0.0;
+        for (int q2 = 0; q2 < gpc; ++q2) sum += red[q2 * m + c2];
+        v = ((i == c2) ? 1.0 : 0.0) - sum;
+        v /= L[i * m + i];
       }
-      Linv[(int64_t)i * m + cc] = v;
+      Linv[(int64_t)i * m + c2] = v;
     }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop, double* __restrict__ Linv,
@@ -139,50 +141,46 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
 }
 
 // ============================================================================ apply: OUT = C · IN
-// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower).  Block: 8 warps × 32 lanes,
-// 128 columns (4 per lane); C staged in smem as fp64.
+// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower), fp64 accumulate.  One CTA per 32 columns:
+// the m_in × 32 slab of IN is staged in shared memory with all loads in flight at once, then warp w
+// computes rows i ≡ w (mod 8) with lane = column (C[i][j] is a warp-uniform broadcast read).
+constexpr int AP_COLS = 32;
 __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
                                                          int64_t d, float* __restrict__ OUT) {
-  extern __shared__ double cs[];                 // 8 rows × m_in (this block's output rows)
-  const int r0 = blockIdx.y * 8;
-  const int nr = min(8, rows - r0);
-  for (int e = threadIdx.x; e < nr * m_in; e += blockDim.x)
-    cs[e] = C[(int64_t)(r0 + e / m_in) * ldc + e % m_in];
+  extern __shared__ float ins[];                 // m_in × AP_COLS
+  const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
+  for (int e = threadIdx.x; e < m_in * AP_COLS; e += blockDim.x) {
+    const int j = e / AP_COLS, cl = e % AP_COLS;
+    const int64_t x = x0 + cl;
+    ins[e] = x < d ? IN[(int64_t)j * d + x] : 0.f;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t x0 = (int64_t)blockIdx.x * 128 + lane;
-  if (warp < nr) {
-    const int i = r0 + warp;
-    const double* crow = cs + warp * m_in;
-    int oi = row_map ? row_map[i] : i;
-    if (oi < 0) return;
-    double acc[4] = {0, 0, 0, 0};
-    int jend = lower ? i + 1 : m_in;
-    for (int j = 0; j < jend; ++j) {
-      double cij = crow[j];
-      if (cij == 0.0) continue;
-      const float* in = IN + (int64_t)j * d;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int64_t x = x0 + q * 32;
-        if (x < d) acc[q] = fma(cij, (double)in[x], acc[q]);
-      }
+  const int64_t x = x0 + lane;
+  for (int i = warp; i < rows; i += 8) {
+    const int oi = row_map ? row_map[i] : i;
+    if (oi < 0) continue;
+    const double* crow = C + (int64_t)i * ldc;
+    const int jend = lower ? min(i + 1, m_in) : m_in;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: the FMA latency is hidden
+    int j = 0;
+    for (; j + 4 <= jend; j += 4) {
+      a0 = fma(__ldg(crow + j), (double)ins[j * AP_COLS + lane], a0);
+      a1 = fma(__ldg(crow + j + 1), (double)ins[(j + 1) * AP_COLS + lane], a1);
+      a2 = fma(__ldg(crow + j + 2), (double)ins[(j + 2) * AP_COLS + lane], a2);
+      a3 = fma(__ldg(crow + j + 3), (double)ins[(j + 3) * AP_COLS + lane], a3);
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int64_t x = x0 + q * 32;
-      if (x < d) OUT[(int64_t)oi * d + x] = (float)acc[q];
-    }
+    for (; j < jend; ++j) a0 = fma(__ldg(crow + j), (double)ins[j * AP_COLS + lane], a0);
+    if (x < d) OUT[(int64_t)oi * d + x] = (float)((a0 + a1) + (a2 + a3));
   }
 }
 
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
                               bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  size_t smem = (size_t)8 * m_in * sizeof(double);
-  dim3 grid((unsigned)ceil_div(d, 128), (unsigned)ceil_div(rows, 8));
-  apply_rows_kernel<<<grid, 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
+  size_t smem = (size_t)m_in * AP_COLS * sizeof(float);
+  apply_rows_kernel<<<(unsigned)ceil_div(d, AP_COLS), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
@@ -255,8 +253,8 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
   if (!scr) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ritz::ritz_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(ritz::ritz_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+    cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
     attr = true;
   }
   const size_t smem = ritz::smem_bytes(m);

@@ -1,9 +1,9 @@
 // tc_xw.cuh — kernel A of the tensor-core pass:  Y_t = X_t·W'ᵀ and S += Y_tᵀY_t   (§8 rows a2 / a7).
 //
 // Persistent, one CTA per SM, 128-row tiles (UMMA M = 128), 64-column K chunks (one 128-byte swizzle row).
-// Warp roles (21 warps): 0–3 epilogue (TMEM lane quadrants), 4–19 converters (fp32 X → bf16 hi/lo, 8 rows
-// each; 16 warps × 3 register buffers keep ~64 KB of loads in flight per SM), 20 control (lane 0: W' TMA
-// ring, lane 1: X TMA ring for bf16 X, lane 2: MMA issue; the warp owns TMEM).
+// Warp roles (22 warps): 0–3 epilogue (TMEM lane quadrants), 4–19 converters (fp32 X → bf16 hi/lo, 8 rows
+// each; 16 warps × 3 register buffers keep ~64 KB of loads in flight per SM), 20 W' TMA ring, 21 MMA issue
+// (owns TMEM).  This kernel serves the plain fp32 layout; TMA-staged X runs kernel A2 (tc_xw2.cuh).
 //
 // Precision (measured, profiles/r1_tc_microtest.txt, tests/tc_accum_test.cu):
 //  * kind::tf32 truncates fp32 operands  → operands are bf16 pairs: X = X_hi + X_lo (fp32 X), W = W_hi + W_lo;
@@ -22,8 +22,9 @@ constexpr int NCONV = 16;          // converter warps
 constexpr int RPW = BM / NCONV;    // rows per converter warp per chunk (8)
 constexpr int LPT = RPW / 2;       // float4 loads per converter thread per chunk (4)
 constexpr int W_CONV0 = 4;
-constexpr int W_CTRL = 4 + NCONV;  // 20
-constexpr int NTHREADS = (W_CTRL + 1) * 32;
+constexpr int W_CTRL = 4 + NCONV;  // 20: W' TMA ring (lane 0), bf16 X TMA ring (lane 1)
+constexpr int W_MMA = W_CTRL + 1;  // 21: MMA issue (own warp: a spinning lane must not delay the producers)
+constexpr int NTHREADS = (W_MMA + 1) * 32;
 constexpr int SFLUSH = 8;          // tiles between fp32 → fp64 flushes of the S partial
 constexpr int PF = 0;              // converter L2-prefetch distance in K chunks (measured: prefetching hurts; off)
 constexpr uint32_t XST = BM * 128; // one bf16 X stage (hi or lo)
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
     if (TMAX) tma_prefetch_desc(&tmX);
     if (XM == 2) tma_prefetch_desc(&tmXlo);
   }
-  if (warp == W_CTRL) tmem_alloc<TCOLS>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc<TCOLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -105,8 +106,8 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
   const int64_t t0 = blockIdx.x, tstep = gridDim.x;
   const int64_t nseg = (p.nk + KSEG - 1) / KSEG;    // accumulation segments per tile
 
-  if (warp == W_CTRL) {
-    if (lane == 0) {
+  if (warp == W_CTRL || warp == W_MMA) {
+    if (warp == W_CTRL && lane == 0) {
       // ---------------------------------------------------------------- W' ring (TMA from L2)
       uint32_t it = 0;
       for (int64_t t = t0; t < p.ntiles && !(p.dbg & 32); t += tstep)
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
           mbar_arrive_expect_tx(&wfull[s], WST);
           tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
         }
-    } else if (TMAX && lane == 1) {
+    } else if (TMAX && warp == W_CTRL && lane == 1) {
       // ---------------------------------------------------------------- X ring (bf16 X / split planes by TMA)
       const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
           tma_load_2d_hint(sX + s * XSTG, &tmX, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
           if (XM == 2) tma_load_2d_hint(sX + s * XSTG + XST, &tmXlo, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
         }
-    } else if (lane == 2) {
+    } else if (warp == W_MMA && lane == 0) {
       // ---------------------------------------------------------------- MMA issue (one thread)
       constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, BM, NB, 0, 0);
       constexpr uint32_t ID_HI = idesc(FMT_BF16, FMT_BF16, BM, MP, 0, 0);
@@ -361,5 +362,5 @@ __global__ void __launch_bounds__(ka::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == W_CTRL) tmem_dealloc<TCOLS>(tmem);
+  if (warp == W_MMA) tmem_dealloc<TCOLS>(tmem);
 }
