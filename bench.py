@@ -29,6 +29,9 @@ if ROOT not in sys.path:
 
 METRIC = "X-pass HBM GB/s (% of peak) and pPCA time-to-LCES at 1/2/4/8 B200"
 LCES_TARGET = {"C1": math.pi / 1024, "C3": math.pi / 1024, "C5": math.pi / 8}   # reading R20
+CFG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
+DESCR = {"C1": "tiny planted exp spectrum", "C3": "planted exp spectrum λ_j=e^(-j/20)",
+         "C5": "wide activation-like (Householder r=8, ReLU, λ_j=1/j)"}
 
 
 def _peaks():
@@ -294,8 +297,8 @@ def run_ours(args, w, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": s.dtype, "data": "synthetic",
-        "config": {"workload": f"{w.name} (BASELINE.json configs[2]): planted exp spectrum, n={s.n}, d={s.d}, "
-                               f"{s.dtype}, k={w.k}, l={w.l}, block power priming",
+        "config": {"workload": f"{w.name} (BASELINE.json configs[{CFG_INDEX.get(w.name, '?')}]): {DESCR.get(w.name, '')}, "
+                               f"n={s.n}, d={s.d}, {s.dtype}, k={w.k}, l={w.l}, block power priming",
                    "n": s.n, "d": s.d, "m": w.m, "k": w.k, "priming": w.priming, "pass_impl": plan_impl,
                    "storage": "f32 split (bf16 hi/lo planes, 4 B/elt)" if split else s.dtype,
                    "parallelism": f"dp{world} (contiguous row shards, NCCL all-reduce of Z,S)",

@@ -360,7 +360,8 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   const int64_t ctas = persistent_ctas(c);
   // one work item (d-group × row group) per CTA: the Zᵀ partial stays in TMEM over ~n/(ctas/ndg) rows, so
   // the partials kernel B writes (and reduce_zp reads) are ≈ (ctas/ndg)·d·mp floats
-  int64_t want = std::max<int64_t>(1, ctas / bp.ndg);
+  // (with more d-groups than CTAs, ≥ 4 items per CTA keep the tail short)
+  int64_t want = bp.ndg <= ctas ? std::max<int64_t>(1, ctas / bp.ndg) : ceil_div(4 * ctas, bp.ndg);
   int64_t rpg = ceil_div(ceil_div(n, want), kb::KR) * kb::KR;
   rpg = std::max<int64_t>(rpg, kb::KR);
   bp.rows_per_rg = rpg;
