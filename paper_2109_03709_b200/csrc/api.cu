@@ -312,7 +312,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   float* Z = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
   double* Sbuf = (double*)scratch(c, S_S, (size_t)4 * m * m * sizeof(double));      // S[2], Bm[2]
   double* theta_dev = (double*)scratch(c, S_TC2, (size_t)std::max(1, iters) * m * sizeof(double) + (size_t)m * m * sizeof(double));
-  double* Rdummy = theta_dev + (size_t)std::max(1, iters) * m;
+
   if (!Z || !Sbuf || !theta_dev) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, m, &plan));
@@ -343,7 +343,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       if (st != PPCA_OK) break;
       cudaEventRecord(ev_main[t & 1], c->stream);
       cudaStreamWaitEvent(c->side, ev_main[t & 1], 0);
-      st = ritz_solve(c, S, Bm, m, theta_dev + (size_t)t * m, Rdummy, c->side);
+      st = ritz_solve(c, S, Bm, m, theta_dev + (size_t)t * m, nullptr, c->side);   // values only
       cudaEventRecord(ev_side[t & 1], c->side);
       if (st != PPCA_OK) break;
     }
@@ -379,17 +379,32 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
     PPCA_TRY(init_rows(c, init_seed, W, m, d));
     PPCA_TRY(check_cuda(c, cudaMemsetAsync(vel, 0, (size_t)m * d * sizeof(float), c->stream), "zero velocity"));
   }
-  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, batch / c->world) * m * sizeof(float));
   float* Q = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
   double* P = (double*)scratch(c, S_S, (size_t)m * m * sizeof(double));
-  if (!Y || !Q || !P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (!Q || !P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   int64_t s0 = *step_io;
+  const size_t row_bytes = (size_t)X->ld * elt_size(X->dtype);
   for (int64_t s = s0; s < s0 + steps; ++s) {
     int64_t r0, rows;
     block_range(X, c->world, batch, s, &r0, &rows);
-    PPCA_TRY(xw(c, X, r0, rows, W, m, Y));
-    PPCA_TRY(ytx(c, X, r0, rows, Y, m, Q));
-    PPCA_TRY(yty(c, Y, m, rows, P));
+    // the step's products Q = X_bᵀ(X_b Wᵀ), P = (X_b Wᵀ)ᵀ(X_b Wᵀ) are one streaming pass over the window:
+    // the tensor-core pass (K-split across the SMs for a short window) when the window is large enough
+    ppca_matrix Xw = *X;
+    Xw.data = static_cast<const uint8_t*>(X->data) + (size_t)r0 * row_bytes;
+    Xw.n_local = rows;
+    PassPlan plan;
+    if (pass_prepare(c, &Xw, m, &plan) != PPCA_OK) plan.impl = 1;   // e.g. a short last block
+    plan.precise = true;
+    if (X->dtype == PPCA_F32) plan.impl = 1;   // the converter kernels read X_hi only in product 2
+    if (plan.impl == 2) {
+      PPCA_TRY(pass_power(c, &Xw, &plan, W, m, Q, P));
+    } else {
+      float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, rows) * m * sizeof(float));
+      if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+      PPCA_TRY(xw(c, X, r0, rows, W, m, Y));
+      PPCA_TRY(ytx(c, X, r0, rows, Y, m, Q));
+      PPCA_TRY(yty(c, Y, m, rows, P));
+    }
     PPCA_TRY(allreduce(c, Q, (size_t)m * d, false));
     PPCA_TRY(allreduce(c, P, (size_t)m * m, true));
     if (eigengame)

@@ -63,7 +63,7 @@ enum Slot {
   S_ROWRED,      // per-row reductions
   S_GEN0, S_GEN1, S_GEN2, S_GEN3,  // generator buffers
   S_EVAL,
-  S_TC0, S_TC1, S_TC2,             // tensor-core pass scratch
+  S_TC0, S_TC1, S_TC2, S_TC3, S_TC4,   // tensor-core pass scratch
   S_NTSTAGE,
 };
 

@@ -40,7 +40,8 @@ ppca_status yty(Ctx* c, const float* Y, int m, int64_t rows, double* S) {
 
 
 ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan);
-ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S);
+ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S,
+                          bool precise);
 ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S);
 void pass_tc_release(Ctx* c);
 
@@ -114,7 +115,7 @@ ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n) {
 
 static ppca_status pass_power_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
                                    float* Z, double* S) {
-  if (plan->impl == 2) return pass_tc_power(c, X, plan, W, m, Z, S);
+  if (plan->impl == 2) return pass_tc_power(c, X, plan, W, m, Z, S, plan->precise);
   float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
   if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   if (X->n_local == 0) {

@@ -8,6 +8,7 @@ namespace ppca {
 
 struct PassPlan {
   int impl = 1;
+  bool precise = false;         // product 2 also reads X_lo of a split X (minibatch steps: Q is the update)
   const float* Wop = nullptr;   // fp32 values of the operand rows the last pass actually used
                                 // (W itself for SIMT; RN_bf16(W) for tcgen05) — for the Ritz Gram
 };

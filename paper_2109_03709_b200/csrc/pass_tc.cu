@@ -200,12 +200,13 @@ static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& 
   return PPCA_OK;
 }
 
-template <int MP, bool XBF16>
-static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap& tmX, const KBParams& bp, int grid) {
-  const size_t smem = kb::Cfg<MP>::SMEM;
-  auto kern = xty_tc_kernel<MP, XBF16>;
+template <int MP, bool XBF16, bool XLO>
+static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
+                             const KBParams& bp, int grid) {
+  const size_t smem = kb::Cfg<MP, XLO>::SMEM;
+  auto kern = xty_tc_kernel<MP, XBF16, XLO>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kb::NTHREADS, smem, c->stream>>>(tmYT, tmX, bp);
+  kern<<<grid, kb::NTHREADS, smem, c->stream>>>(tmYT, tmX, tmXlo, bp);
   PPCA_LAUNCH_CHECK(c, "xty_tc_kernel");
   return PPCA_OK;
 }
@@ -253,18 +254,18 @@ static ppca_status dispatch_ka(Ctx* c, int mp, const CUtensorMap& tmW, const CUt
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
 
-template <bool XBF16>
-static ppca_status dispatch_kb(Ctx* c, int mp, const CUtensorMap& tmYT, const CUtensorMap& tmX, const KBParams& bp,
-                               int grid) {
+template <bool XBF16, bool XLO>
+static ppca_status dispatch_kb(Ctx* c, int mp, const CUtensorMap& tmYT, const CUtensorMap& tmX,
+                               const CUtensorMap& tmXlo, const KBParams& bp, int grid) {
   switch (mp) {
-    case 16: return launch_kb<16, XBF16>(c, tmYT, tmX, bp, grid);
-    case 32: return launch_kb<32, XBF16>(c, tmYT, tmX, bp, grid);
-    case 48: return launch_kb<48, XBF16>(c, tmYT, tmX, bp, grid);
-    case 64: return launch_kb<64, XBF16>(c, tmYT, tmX, bp, grid);
-    case 80: return launch_kb<80, XBF16>(c, tmYT, tmX, bp, grid);
-    case 96: return launch_kb<96, XBF16>(c, tmYT, tmX, bp, grid);
-    case 112: return launch_kb<112, XBF16>(c, tmYT, tmX, bp, grid);
-    case 128: return launch_kb<128, XBF16>(c, tmYT, tmX, bp, grid);
+    case 16: return launch_kb<16, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 32: return launch_kb<32, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 48: return launch_kb<48, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 64: return launch_kb<64, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 80: return launch_kb<80, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 96: return launch_kb<96, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 112: return launch_kb<112, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 128: return launch_kb<128, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
   }
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
@@ -300,7 +301,7 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
 }
 
 static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, int mp, double* S,
-                          __nv_bfloat16* YT, int64_t ldyt) {
+                          __nv_bfloat16* YT, int64_t ldyt, int ksplit = 1, float* Ypart = nullptr) {
   CUtensorMap tmW, tmX, tmXlo;
   if (!make_map_bf16(&tmW, Wb, X->d, 2 * mp, X->d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
   tmX = tmXlo = tmW;   // unused unless X is staged by TMA
@@ -310,10 +311,13 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   kp.ntiles = ceil_div(X->n_local, ka::BM);
   kp.nk = ceil_div(X->d, ka::BK);
   kp.YT = YT; kp.ldyt = ldyt;
+  kp.ksplit = ksplit;
+  kp.kper = ceil_div(kp.nk, (int64_t)ksplit);
+  kp.Ypart = Ypart;
   static int dbg = -1;
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   kp.dbg = dbg;
-  int grid = (int)std::min<int64_t>(persistent_ctas(c), kp.ntiles);
+  int grid = (int)std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit);
   // TMA-staged X (bf16, split) runs kernel A2; its S partial has 2·mp rows when S is on the tensor cores
   const bool tma_x = X->dtype != PPCA_F32;
   const bool smma = tma_x && mp == 64;
@@ -323,6 +327,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka2<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
            : X->dtype == PPCA_F32_SPLIT ? dispatch_ka2<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
                                         : dispatch_ka<0>(c, mp, tmW, tmX, tmXlo, kp, grid));
+  if (ksplit > 1) return PPCA_OK;                 // partial Y out; the caller forms S from the summed Y
   if (smma)
     reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
   else
@@ -340,7 +345,36 @@ ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, con
   return run_ka(c, X, Wb, m, mp, S, nullptr, 0);
 }
 
-ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S) {
+// Y of a K-split row window: Y = Σ_parts Ypart (fixed order) → Yᵀ bf16 pair [2·mp][ldyt] (rows ≥ n zero)
+// and the compact fp32 Y [n][m] for S = YᵀY.
+__global__ void ysum_kernel(const float* __restrict__ Ypart, int ksplit, int64_t n, int mp, int m,
+                            __nv_bfloat16* __restrict__ YT, int64_t ldyt, float* __restrict__ Yc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)mp * ldyt) return;
+  const int j = (int)(e / ldyt);
+  const int64_t r = e % ldyt;
+  float y = 0.f;
+  if (r < n)
+    for (int q = 0; q < ksplit; ++q) y += Ypart[((int64_t)q * n + r) * mp + j];
+  const __nv_bfloat16 hi = __float2bfloat16_rn(y);
+  YT[(int64_t)j * ldyt + r] = hi;
+  YT[(int64_t)(mp + j) * ldyt + r] = __float2bfloat16_rn(y - __bfloat162float(hi));
+  if (r < n && j < m) Yc[r * m + j] = y;
+}
+
+// K split for short row windows (a minibatch step): enough (tile, K part) items to cover the SMs
+static int pick_ksplit(const Ctx* c, const ppca_matrix* X, int64_t nk) {
+  if (X->dtype == PPCA_F32) return 1;                 // the converter kernel A has no K split
+  const int64_t ntiles = ceil_div(X->n_local, ka::BM);
+  const int64_t ctas = persistent_ctas(c);
+  if (2 * ntiles > ctas) return 1;
+  int64_t ks = std::min<int64_t>(nk, std::max<int64_t>(1, ctas / ntiles));
+  const int64_t kper = ceil_div(nk, ks);
+  return (int)ceil_div(nk, kper);
+}
+
+ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S,
+                          bool precise) {
   const int mp = pad16(m);
   const int64_t n = X->n_local, d = X->d;
   __nv_bfloat16* Wb;
@@ -351,7 +385,19 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   const int64_t ldyt = ceil_div(n, 64) * 64;
   __nv_bfloat16* YT = (__nv_bfloat16*)scratch(c, S_Y, (size_t)2 * mp * ldyt * 2);
   if (!YT) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  PPCA_TRY(run_ka(c, X, Wb, m, mp, S, YT, ldyt));
+  const int64_t nk = ceil_div(d, ka::BK);
+  const int ksplit = pick_ksplit(c, X, nk);
+  if (ksplit == 1) {
+    PPCA_TRY(run_ka(c, X, Wb, m, mp, S, YT, ldyt));
+  } else {
+    float* Ypart = (float*)scratch(c, S_TC3, (size_t)ksplit * n * mp * sizeof(float));
+    float* Yc = (float*)scratch(c, S_TC4, (size_t)n * m * sizeof(float));
+    if (!Ypart || !Yc) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    PPCA_TRY(run_ka(c, X, Wb, m, mp, S, nullptr, 0, ksplit, Ypart));
+    ysum_kernel<<<(unsigned)ceil_div((int64_t)mp * ldyt, 256), 256, 0, c->stream>>>(Ypart, ksplit, n, mp, m, YT, ldyt, Yc);
+    PPCA_LAUNCH_CHECK(c, "ysum");
+    PPCA_TRY(yty(c, Yc, m, n, S));
+  }
   // kernel B
   const int nc = mp <= 64 ? 2 : 1;
   KBParams bp;
@@ -376,7 +422,12 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   // product 2 reads X_hi only: bf16 X, or the hi plane of a split X, by TMA
   if (X->dtype != PPCA_F32 && !make_x_maps(X, kb::KR, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   const int grid = (int)std::min<int64_t>(ctas, bp.ndg * bp.nrg);
-  PPCA_TRY(X->dtype != PPCA_F32 ? dispatch_kb<true>(c, mp, tmYT, tmX, bp, grid) : dispatch_kb<false>(c, mp, tmYT, tmX, bp, grid));
+  if (X->dtype == PPCA_F32)
+    PPCA_TRY((dispatch_kb<false, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
+  else if (precise && X->dtype == PPCA_F32_SPLIT)
+    PPCA_TRY((dispatch_kb<true, true>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
+  else
+    PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;

@@ -22,10 +22,12 @@ __device__ __forceinline__ void pair_of(int r, int i, int mm, int& p, int& q) {
   q = a < b ? b : a;
 }
 
+// R == nullptr: eigenvalues only (the per-iterate θ history of power priming) — no V accumulation.
 template <typename VT>
 __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S, const double* __restrict__ Bm, int m,
                                                    double* __restrict__ gLinv, double* __restrict__ gT1,
                                                    double* __restrict__ theta, double* __restrict__ R, int* d_err) {
+  const bool vectors = R != nullptr;
   extern __shared__ double sm[];
   const int mm = (m + 1) & ~1;          // even (a dummy player for odd m)
   const int np = mm / 2;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
       A[i * mm + j] = v;
       A[j * mm + i] = v;
     }
-    V[e] = (VT)(i == j ? 1.0 : 0.0);
+    if (vectors) V[e] = (VT)(i == j ? 1.0 : 0.0);
   }
   __syncthreads();
   // 3. Jacobi sweeps
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
         A[q * mm + p2] = c2 * rc - s2 * rd;
         A[q * mm + q2] = s2 * rc + c2 * rd;
       }
-      for (int e = tid; e < np * mm; e += nt) {        // V stored transposed: V[col·mm + row]
+      for (int e = tid; e < (vectors ? np * mm : 0); e += nt) {   // V stored transposed: V[col·mm + row]
         const int ia = e / mm, row = e % mm;
         const int p = pq[2 * ia], q = pq[2 * ia + 1];
         const double cc = csn[2 * ia], ss = csn[2 * ia + 1];
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
   }
   __syncthreads();
   for (int i = tid; i < m; i += nt) theta[i] = A[perm[i] * mm + perm[i]];
-  for (int e = tid; e < m * m; e += nt) {
+  for (int e = tid; e < (vectors ? m * m : 0); e += nt) {
     const int i = e / m, j = e % m;
     const int col = perm[i];
     double s = 0.0;

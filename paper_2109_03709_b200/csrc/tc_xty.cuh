@@ -16,14 +16,18 @@ constexpr int PF = 0;           // converter L2-prefetch distance in half-stages
 constexpr int W_CONV0 = 4, W_PROD = 12, W_MMA = 13;
 constexpr int NTHREADS = 14 * 32;
 constexpr uint32_t BLK = KR * 128;            // one 64-column block of a stage (bytes)
-template <int MP> struct Cfg {
+// XLO: the X_lo plane of a split X is staged too and X_loᵀ·Y_hi is added (the minibatch steps, whose
+// products are the update itself; the power pass reads X_hi only)
+template <int MP, bool XLO = false> struct Cfg {
   static constexpr int NC = MP <= 64 ? 2 : 1;             // 128-wide d chunks per work item
   static constexpr int NB = 2 * MP;                      // UMMA N: [Y_hi; Y_lo]
-  static constexpr uint32_t XST = NC * 2 * BLK;          // X stage bytes
+  static constexpr uint32_t XST = NC * 2 * BLK;          // X stage bytes (one plane)
+  static constexpr uint32_t XSTG = XLO ? 2 * XST : XST;  // X stage bytes (all planes)
   static constexpr uint32_t YST = NB * 128;              // Yᵀ stage bytes (NB rows × 64 K)
   static constexpr uint32_t ACC = NC * NB;               // TMEM columns per accumulator buffer
   static constexpr uint32_t TCOLS = 2 * ACC <= 64 ? 64 : (2 * ACC <= 128 ? 128 : (2 * ACC <= 256 ? 256 : 512));
-  static constexpr size_t SMEM = 1024 + NST * (XST + YST) + 256;
+  static constexpr int NSTG = XLO ? (int)((227 * 1024 - 1280) / (XSTG + YST)) : NST;
+  static constexpr size_t SMEM = 1024 + NSTG * (XSTG + YST) + 256;
 };
 }  // namespace kb
 
@@ -37,13 +41,15 @@ struct KBParams {
   float* Zp;                // [nrg][d_pad][mp] fp32 partials (d_pad = ndg·NC·128)
 };
 
-template <int MP, bool XBF16>
+template <int MP, bool XBF16, bool XLO = false>
 __global__ void __launch_bounds__(kb::NTHREADS, 1)
-    xty_tc_kernel(const __grid_constant__ CUtensorMap tmYT, const __grid_constant__ CUtensorMap tmX, KBParams p) {
+    xty_tc_kernel(const __grid_constant__ CUtensorMap tmYT, const __grid_constant__ CUtensorMap tmX,
+                  const __grid_constant__ CUtensorMap tmXlo, KBParams p) {
   using namespace kb;
-  using CF = Cfg<MP>;
-  constexpr int NC = CF::NC, NB = CF::NB;
-  constexpr uint32_t XST = CF::XST, YST = CF::YST, ACC = CF::ACC, TCOLS = CF::TCOLS;
+  using CF = Cfg<MP, XLO>;
+  constexpr int NC = CF::NC, NB = CF::NB, NST = CF::NSTG;
+  constexpr uint32_t XST = CF::XSTG, XPL = CF::XST, YST = CF::YST, ACC = CF::ACC, TCOLS = CF::TCOLS;
+  static_assert(!XLO || XBF16, "the X_lo plane is staged by TMA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sX = sm;
@@ -69,6 +75,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
   if (warp == W_PROD && lane == 0) {
     tma_prefetch_desc(&tmYT);
     if (XBF16) tma_prefetch_desc(&tmX);
+    if (XLO) tma_prefetch_desc(&tmXlo);
   }
   if (warp == W_MMA) tmem_alloc<TCOLS>(tmem_slot);
   tc_fence_before();
@@ -100,11 +107,16 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
             for (int bl = 0; bl < NC * 2; ++bl)
               tma_load_2d_hint(sX + s * XST + bl * BLK, &tmX, &full[s], (int32_t)(c0 + bl * 64),
                                (int32_t)(r0 + ks * KR), pol);
+          if (XLO)
+            for (int bl = 0; bl < NC * 2; ++bl)
+              tma_load_2d_hint(sX + s * XST + XPL + bl * BLK, &tmXlo, &full[s], (int32_t)(c0 + bl * 64),
+                               (int32_t)(r0 + ks * KR), pol);
         }
       }
     }
   } else if (warp == W_MMA) {
     constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, 128, NB, 1, 0);    // A = Xᵀ MN-major, B = Yᵀ K-major
+    constexpr uint32_t ID_HI = idesc(FMT_BF16, FMT_BF16, 128, MP, 1, 0);  // X_loᵀ·Y_hi into the hi columns
     uint32_t it = 0, tt = 0;
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++tt) {
       int64_t r0, nks;
@@ -122,8 +134,13 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
           for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int kk = 0; kk < KR / 16; ++kk)
+            {
               mma_bf16(tmem + b * ACC + c * NB, smem_desc_sw128(xa + c * 2 * BLK + kk * 2048, BLK, 1024),
                        smem_desc_sw128(ya + kk * 32, 16, 1024), ID, (ks | kk) != 0);
+              if (XLO)
+                mma_bf16(tmem + b * ACC + c * NB, smem_desc_sw128(xa + XPL + c * 2 * BLK + kk * 2048, BLK, 1024),
+                         smem_desc_sw128(ya + kk * 32, 16, 1024), ID_HI, 1);
+            }
           mma_commit(&empty[s]);
         }
         __syncwarp();

@@ -47,6 +47,11 @@ struct KAParams {
   int64_t ldyt;
   double* Spart;          // [gridDim.x][mp][mp] fp64 per-CTA partials (upper triangle used)
   int dbg;                // experiment switches (env PPCA_DBG; 0 in production)
+  // K split (kernel A2 only): work item = (tile, K part); with ksplit > 1 the epilogue writes the fp32
+  // partial Y of its K part to Ypart [ksplit][n][mp] (no S, no Yᵀ) for a short row window (minibatch step)
+  int ksplit = 1;
+  int64_t kper = 0;       // K chunks per part
+  float* Ypart = nullptr;
 };
 
 template <int MP, int XM>

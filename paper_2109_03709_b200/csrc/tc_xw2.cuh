@@ -112,44 +112,46 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t t0 = blockIdx.x, tstep = gridDim.x;
-  const int64_t nseg = (p.nk + KSEG - 1) / KSEG;
+  // work item = (row tile, K part): t = it / ksplit, chunks [k0, k1) (ksplit = 1: whole tiles)
+  const int64_t nitems = p.ntiles * p.ksplit, i0 = blockIdx.x, istep = gridDim.x;
+  const bool partial = p.ksplit > 1;
+  auto item = [&](int64_t it, int64_t& t, int64_t& k0, int64_t& k1, int64_t& nseg) {
+    t = it / p.ksplit;
+    k0 = (it % p.ksplit) * p.kper;
+    k1 = min(p.nk, k0 + p.kper);
+    nseg = k1 > k0 ? (k1 - k0 + KSEG - 1) / KSEG : 0;
+  };
 
   if (warp >= W_WPROD) {
     if (warp == W_WPROD && lane == 0) {
       // ---------------------------------------------------------------- W' ring (TMA, L2-resident)
       uint32_t it = 0;
-      for (int64_t t = t0; t < p.ntiles && !(p.dbg & 32); t += tstep)
-        for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
+      for (int64_t wi = i0; wi < nitems && !(p.dbg & 32); wi += istep) {
+        int64_t t, k0, k1, ns;
+        item(wi, t, k0, k1, ns);
+        for (int64_t kc = k0; kc < k1; ++kc, ++it) {
           const uint32_t s = it % NWS, ph = (it / NWS) & 1;
           mbar_wait(&wempty[s], ph ^ 1);
           mbar_arrive_expect_tx(&wfull[s], WST);
           tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
         }
+      }
     } else if (warp == W_XPROD && lane == 0) {
       // ---------------------------------------------------------------- X ring (hi [+ lo] planes)
       const uint64_t pol = policy_evict_first();
-      // L2 prefetch cursor PFD chunks ahead of the loads (PPCA_DBG bit 128 disables it)
-      const int PFD = (p.dbg & 128) ? 0 : XPF;
-      int64_t pt = t0, pk = 0;
-      auto prefetch = [&]() {
-        if (pt >= p.ntiles) return;
-        tma_prefetch_2d(&tmX, (int32_t)(pk * BK), (int32_t)(pt * BM));
-        if (LO) tma_prefetch_2d(&tmXlo, (int32_t)(pk * BK), (int32_t)(pt * BM));
-        if (++pk == p.nk) { pk = 0; pt += tstep; }
-      };
-      for (int i = 0; i < PFD; ++i) prefetch();
       uint32_t it = 0;
-      for (int64_t t = t0; t < p.ntiles; t += tstep)
-        for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
+      for (int64_t xi = i0; xi < nitems; xi += istep) {
+        int64_t t, k0, k1, ns;
+        item(xi, t, k0, k1, ns);
+        for (int64_t kc = k0; kc < k1; ++kc, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
-          if (PFD) prefetch();
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], (p.dbg & 64) ? XST : XSTG);
           tma_load_2d_hint(sX + s * XSTG, &tmX, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
           if (LO && !(p.dbg & 64))
             tma_load_2d_hint(sX + s * XSTG + XST, &tmXlo, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
         }
+      }
     } else if (warp == W_MMA && lane == 0) {
       // ---------------------------------------------------------------- MMA issue (one thread)
       constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, BM, NB, 0, 0);
@@ -167,14 +169,16 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         mma_commit(sfull);
       };
       uint32_t it = 0, sg = 0, lt = 0;
-      for (int64_t t = t0; t < p.ntiles; t += tstep, ++lt) {
+      for (int64_t mi = i0; mi < nitems; mi += istep, ++lt) {
+        int64_t t, k0, k1, nseg;
+        item(mi, t, k0, k1, nseg);
         for (int64_t g = 0; g < nseg; ++g, ++sg) {
           const uint32_t b = sg % NTB, tph = (sg / NTB) & 1;
           mbar_wait(&tempty[b], tph ^ 1);
           tc_fence_after();
           const uint32_t dcol = tmem + b * NB;
-          const int64_t k1 = min(p.nk, (g + 1) * KSEG);
-          for (int64_t kc = g * KSEG; kc < k1; ++kc, ++it) {
+          const int64_t g0 = k0 + g * KSEG, g1 = min(k1, g0 + KSEG);
+          for (int64_t kc = g0; kc < g1; ++kc, ++it) {
             const uint32_t s = it % NST, ph = (it / NST) & 1;
             const uint32_t ws = it % NWS, wph = (it / NWS) & 1;
             if (!(p.dbg & 32)) mbar_wait(&wfull[ws], wph);
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 16 && !(p.dbg & 1); ++kk) {
               mma_bf16(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024), ID,
-                       (kc != g * KSEG) || kk != 0);
+                       (kc != g0) || kk != 0);
               if (LO)
                 mma_bf16(dcol, smem_desc_sw128(xa + XST + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024),
                          ID_HI, 1);
@@ -196,9 +200,9 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         }
         // S of the previous tile, issued behind this tile's product 1 so the tensor pipe never waits
         // for the epilogue
-        if (SMMA && lt > 0) issue_s(lt - 1);
+        if (SMMA && !partial && lt > 0) issue_s(lt - 1);
       }
-      if (SMMA && lt > 0) issue_s(lt - 1);
+      if (SMMA && !partial && lt > 0) issue_s(lt - 1);
     }
   } else {
     // ------------------------------------------------------------------ epilogue (128 threads = 128 rows)
@@ -237,8 +241,12 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         }
         if (++pending == SFLUSH) flush();
       };
-      for (int64_t t = t0; t < p.ntiles; t += tstep, ++lt) {
+      for (int64_t ei = i0; ei < nitems; ei += istep) {
+        int64_t t, k0, k1, nseg;
+        item(ei, t, k0, k1, nseg);
         float y[MP];
+#pragma unroll
+        for (int j = 0; j < MP; ++j) y[j] = 0.f;
         for (int64_t g = 0; g < nseg; ++g, ++sg) {
           const uint32_t b = sg % NTB, tph = (sg / NTB) & 1;
           mbar_wait(&tfull[b], tph);
@@ -249,13 +257,21 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
             tmem_ld8(tmem + tl + b * NB + c0, v);        // X'·W_hiᵀ
             tmem_ld8(tmem + tl + b * NB + MP + c0, w);   // X'·W_loᵀ
 #pragma unroll
-            for (int j = 0; j < 8; ++j) y[c0 + j] = (g == 0 ? 0.f : y[c0 + j]) + (v[j] + w[j]);
+            for (int j = 0; j < 8; ++j) y[c0 + j] = y[c0 + j] + (v[j] + w[j]);
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[b]);
         }
         const int64_t grow = t * BM + tid;
+        if (partial) {                                   // K part of a row window: fp32 partial Y out
+          if (grow < p.n) {
+            float4* dst = reinterpret_cast<float4*>(p.Ypart + ((ei % p.ksplit) * p.n + grow) * MP);
+#pragma unroll
+            for (int j = 0; j < MP; j += 4) dst[j / 4] = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+          }
+          continue;
+        }
         if (p.YT && grow < p.ldyt) {                     // Yᵀ as a bf16 pair [Y_hi; Y_lo] (rows ≥ n are zero)
 #pragma unroll
           for (int j = 0; j < MP; ++j) {
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(yfull);
+        ++lt;
       }
       if (lt > 0) drain(lt - 1);
       if (pending) flush();
@@ -304,7 +321,11 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           bj_[q] = bi + b;
         }
       }
-      for (int64_t t = t0; t < p.ntiles; t += tstep, ++lt) {
+      for (int64_t ei = i0; ei < nitems; ei += istep, ++lt) {
+        int64_t t, k0, k1, nseg;
+        item(ei, t, k0, k1, nseg);
+        if (nseg == 0)
+          for (int j = 0; j < MP; ++j) yrow[j] = 0.f;
         for (int64_t g = 0; g < nseg; ++g, ++sg) {
           const uint32_t b = sg % NTB, tph = (sg / NTB) & 1;
           mbar_wait(&tfull[b], tph);
@@ -322,6 +343,13 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           if (lane == 0) mbar_arrive(&tempty[b]);
         }
         const int64_t grow = t * BM + tid;
+        if (partial) {
+          if (grow < p.n) {
+            float4* dst = reinterpret_cast<float4*>(p.Ypart + ((ei % p.ksplit) * p.n + grow) * MP);
+            for (int j = 0; j < MP; j += 4) dst[j / 4] = *reinterpret_cast<const float4*>(yrow + j);
+          }
+          continue;
+        }
         if (p.YT && grow < p.ldyt) {
 #pragma unroll 4
           for (int j = 0; j < MP; ++j) {

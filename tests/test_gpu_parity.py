@@ -186,8 +186,9 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
 
 
 # ----------------------------------------------------------------------------- minibatch primings
+@pytest.mark.parametrize("impl", [0, 2], indirect=True, ids=["auto", "tcgen05"])
 @pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
-def test_oja_parity_c2s(P, ctx, split):
+def test_oja_parity_c2s(P, ctx, split, impl):
     import torch
     w = C.SMALL["C2s"]
     s = w.spec
@@ -203,14 +204,16 @@ def test_oja_parity_c2s(P, ctx, split):
     assert nxt == steps
     Wh = W.cpu().numpy().astype(np.float64)
     rel = np.linalg.norm(Wh - W_ref) / np.linalg.norm(W_ref)
+    print(f"\n[parity] C2s oja split={split} impl={impl}: trajectory drift {rel:.2e}")
     assert rel < 1e-3, f"Oja trajectory drift {rel:.2e}"
     E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
     th, dim = P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), "C2s", th_all_ref)
 
 
+@pytest.mark.parametrize("impl", [0, 2], indirect=True, ids=["auto", "tcgen05"])
 @pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
-def test_eigengame_parity_c4s(P, ctx, split):
+def test_eigengame_parity_c4s(P, ctx, split, impl):
     import torch
     w = C.SMALL["C4s"]
     s = w.spec
@@ -223,9 +226,12 @@ def test_eigengame_parity_c4s(P, ctx, split):
     V = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
     vel = torch.zeros_like(V)
     P.ppca_prime_eigengame(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, w.init_seed, V, vel, 0)
+    if impl == 2 and split:
+        assert P.ppca_last_pass_impl(ctx) == 2          # the step's products ran on the tensor cores
     Vh = V.cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(np.linalg.norm(Vh, axis=1), 1, atol=1e-5)
     rel = np.linalg.norm(Vh - V_ref) / np.linalg.norm(V_ref)
+    print(f"\n[parity] C4s eigengame split={split} impl={impl}: trajectory drift {rel:.2e}")
     assert rel < 1e-3, f"EigenGame trajectory drift {rel:.2e}"
     E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
     th, dim = P.ppca_refine(ctx, Xm, V, w.m, w.k, E)
