@@ -141,16 +141,19 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
 }
 
 // ============================================================================ apply: OUT = C · IN
-// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower), fp64 accumulate.  One CTA per 32 columns:
-// the m_in × 32 slab of IN is staged in shared memory with all loads in flight at once, then warp w
-// computes rows i ≡ w (mod 8) with lane = column (C[i][j] is a warp-uniform broadcast read).
+// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower), fp64 accumulate.  One CTA per 32 columns: the
+// rows × m_in block of C (fp64) and the m_in × 32 slab of IN are staged in shared memory with every load
+// in flight at once (the inner loop then never waits on L2), warp w computes rows i ≡ w (mod 8) with
+// lane = column (C[i][j] a shared-memory broadcast).
 constexpr int AP_COLS = 32;
 __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
                                                          int64_t d, float* __restrict__ OUT) {
-  extern __shared__ float ins[];                 // m_in × AP_COLS
+  extern __shared__ double cs[];                 // rows × m_in (fp64), then m_in × AP_COLS (fp32)
+  float* ins = reinterpret_cast<float*>(cs + (size_t)rows * m_in);
   const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
+  for (int e = threadIdx.x; e < rows * m_in; e += blockDim.x) cs[e] = C[(int64_t)(e / m_in) * ldc + e % m_in];
   for (int e = threadIdx.x; e < m_in * AP_COLS; e += blockDim.x) {
     const int j = e / AP_COLS, cl = e % AP_COLS;
     const int64_t x = x0 + cl;
@@ -162,24 +165,29 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
   for (int i = warp; i < rows; i += 8) {
     const int oi = row_map ? row_map[i] : i;
     if (oi < 0) continue;
-    const double* crow = C + (int64_t)i * ldc;
+    const double* crow = cs + (size_t)i * m_in;
     const int jend = lower ? min(i + 1, m_in) : m_in;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: the FMA latency is hidden
     int j = 0;
     for (; j + 4 <= jend; j += 4) {
-      a0 = fma(__ldg(crow + j), (double)ins[j * AP_COLS + lane], a0);
-      a1 = fma(__ldg(crow + j + 1), (double)ins[(j + 1) * AP_COLS + lane], a1);
-      a2 = fma(__ldg(crow + j + 2), (double)ins[(j + 2) * AP_COLS + lane], a2);
-      a3 = fma(__ldg(crow + j + 3), (double)ins[(j + 3) * AP_COLS + lane], a3);
+      a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
+      a1 = fma(crow[j + 1], (double)ins[(j + 1) * AP_COLS + lane], a1);
+      a2 = fma(crow[j + 2], (double)ins[(j + 2) * AP_COLS + lane], a2);
+      a3 = fma(crow[j + 3], (double)ins[(j + 3) * AP_COLS + lane], a3);
     }
-    for (; j < jend; ++j) a0 = fma(__ldg(crow + j), (double)ins[j * AP_COLS + lane], a0);
+    for (; j < jend; ++j) a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
     if (x < d) OUT[(int64_t)oi * d + x] = (float)((a0 + a1) + (a2 + a3));
   }
 }
 
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
                               bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  size_t smem = (size_t)m_in * AP_COLS * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  size_t smem = (size_t)rows * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
   apply_rows_kernel<<<(unsigned)ceil_div(d, AP_COLS), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
@@ -386,31 +394,41 @@ ppca_status oja_update(Ctx* c, const float* Q, const double* P, float* W, float*
 }
 
 // EigenGame coefficients from A (m×m): Cf[j][i] = A_ji / A_ii (i < j), twoU[j] = 2(A_jj − Σ_{i<j} A_ji²/A_ii).
-__global__ void eg_coeff_kernel(const double* __restrict__ A, int m, double* __restrict__ Cf,
-                                double* __restrict__ twoU, int* d_err) {
+// One CTA: diagonal reciprocals in shared memory, then warp-per-j rows (lanes over i, fixed-order sums).
+__global__ void __launch_bounds__(256) eg_coeff_kernel(const double* __restrict__ A, int m, double* __restrict__ Cf,
+                                                       double* __restrict__ twoU, int* d_err) {
+  __shared__ double rdiag[PPCA_MAX_M];
   __shared__ double amax;
-  if (threadIdx.x == 0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
     double mx = 0.0;
-    for (int i = 0; i < m; ++i) mx = fmax(mx, A[i * m + i]);
-    amax = mx;
+    for (int i = lane; i < m; i += 32) mx = fmax(mx, A[i * m + i]);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) amax = mx;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    double u = A[j * m + j];
-    for (int i = 0; i < m; ++i) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double aii = A[i * m + i];
+    if (!(aii > 1e-12 * amax)) {
+      atomicOr(d_err, DEV_DEGENERATE);
+      aii = 1.0;
+    }
+    rdiag[i] = 1.0 / aii;
+  }
+  __syncthreads();
+  for (int j = warp; j < m; j += blockDim.x >> 5) {
+    double part = 0.0;
+    for (int i = lane; i < m; i += 32) {
       double cf = 0.0;
       if (i < j) {
-        double aii = A[i * m + i];
-        if (!(aii > 1e-12 * amax)) {
-          atomicOr(d_err, DEV_DEGENERATE);
-          aii = 1.0;
-        }
-        cf = A[j * m + i] / aii;
-        u -= A[j * m + i] * cf;
+        const double aji = A[j * m + i];
+        cf = aji * rdiag[i];
+        part += aji * cf;
       }
       Cf[j * m + i] = cf;
     }
-    twoU[j] = 2.0 * u;
+    part = warp_sum(part);
+    if (lane == 0) twoU[j] = 2.0 * (A[j * m + j] - part);
   }
 }
 
@@ -434,7 +452,7 @@ ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V,
   double* Cf = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + (size_t)m * sizeof(double) + 64);
   double* twoU = Cf + (size_t)m * m;
   float* T = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
-  eg_coeff_kernel<<<1, 128, 0, c->stream>>>(A, m, Cf, twoU, c->d_err);
+  eg_coeff_kernel<<<1, 256, 0, c->stream>>>(A, m, Cf, twoU, c->d_err);
   PPCA_LAUNCH_CHECK(c, "eg_coeff");
   PPCA_TRY(apply_rows(c, Cf, m, m, m, nullptr, false, MV, d, T, c->stream));
   int64_t count = (int64_t)m * d;
