@@ -79,10 +79,12 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
     // phase 2: write column j, update the trailing lower triangle A[i][k] -= l_i l_k (k ≤ i)
     for (int i = j + tid; i < m; i += nt) A[i * m + j] = colj[i];
     if (!dr) {
-      const int rem = m - j - 1;
-      for (int e = tid; e < rem * rem; e += nt) {
-        const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-        if (k <= i) A[i * m + k] -= colj[i] * colj[k];
+      // 2-D thread map (no integer division in the loop): rows i ≡ ty, columns k ≡ tx (mod 16), k ≤ i
+      const int ty = tid >> 4, tx = tid & 15, sy = nt >> 4;
+      for (int i = j + 1 + ty; i < m; i += sy) {
+        const double li = colj[i];
+        double* Ai = A + i * m;
+        for (int k = j + 1 + tx; k <= i; k += 16) Ai[k] -= li * colj[k];
       }
     }
     __syncthreads();
@@ -98,8 +100,16 @@ __device__ void block_lower_inverse(const double* L, int m, const int* keep, dou
   const int cc = tid % m, q = tid / m;
   for (int i = 0; i < m; ++i) {
     double part = 0.0;
-    if (q < gpc && cc < i && keep[i])
-      for (int j = cc + q; j < i; j += gpc) part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
+    if (q < gpc && cc < i && keep[i]) {
+      double p2 = 0.0;                         // two chains: half the dependent-FMA latency
+      int j = cc + q;
+      for (; j + gpc < i; j += 2 * gpc) {
+        part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
+        p2 = fma(L[i * m + j + gpc], Linv[(int64_t)(j + gpc) * m + cc], p2);
+      }
+      if (j < i) part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
+      part += p2;
+    }
     if (q < gpc) red[q * m + cc] = part;
     __syncthreads();
     for (int c2 = tid; c2 < m; c2 += nt) {
