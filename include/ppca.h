@@ -191,6 +191,11 @@ ppca_status ppca_philox_words(ppca_ctx* ctx, uint64_t seed, uint32_t stream, uin
 ppca_status ppca_set_timing(ppca_ctx* ctx, int enable);
 ppca_status ppca_get_pass_time(ppca_ctx* ctx, double* ms_total, int64_t* passes);
 
+/* Timing hook (bench.py roofline of the dominant kernel): with timing enabled, each launch of the
+ * tensor-core kernel A (which = 0: Y = X·W'ᵀ, S = YᵀY) and kernel B (which = 1: Zᵀ = XᵀY) is bracketed by
+ * CUDA events on the context stream; returns the summed device time (ms) and launch count, then resets. */
+ppca_status ppca_get_kernel_time(ppca_ctx* ctx, int which, double* ms_total, int64_t* launches);
+
 /* Timing hook: select the fused-pass implementation (0 = auto, 1 = SIMT fp32, 2 = tcgen05).
  * Returns UNSUPPORTED if the requested path cannot run this matrix. */
 ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);

@@ -30,7 +30,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl", "ppca_split_f32"]
+           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time"]
 
 
 class PPCAError(RuntimeError):
@@ -90,6 +90,7 @@ def load(path: str = LIB_PATH):
         "ppca_last_pass_impl": (I, [P]),
         "ppca_get_pass_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "ppca_split_f32": (I, [P, P, I64, I64, I64]),
+        "ppca_get_kernel_time": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -241,6 +242,13 @@ def ppca_set_timing(ctx, enable: bool) -> None:
 def ppca_get_pass_time(ctx) -> tuple[float, int]:
     ms, n = ctypes.c_double(), ctypes.c_int64()
     _check(ctx, load().ppca_get_pass_time(ctx, ctypes.byref(ms), ctypes.byref(n)), "ppca_get_pass_time")
+    return ms.value, n.value
+
+
+def ppca_get_kernel_time(ctx, which: int) -> tuple[float, int]:
+    """(summed ms, launches) of tensor-core kernel A (which=0) or B (which=1) since the last call."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    _check(ctx, load().ppca_get_kernel_time(ctx, which, ctypes.byref(ms), ctypes.byref(n)), "ppca_get_kernel_time")
     return ms.value, n.value
 
 

@@ -249,6 +249,7 @@ ppca_status ppca_set_timing(ppca_ctx* h, int enable) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   h->c.timing = enable != 0;
   h->c.tev_used = 0;
+  h->c.kev_used[0] = h->c.kev_used[1] = 0;
   return PPCA_OK;
 }
 
@@ -256,6 +257,12 @@ ppca_status ppca_get_pass_time(ppca_ctx* h, double* ms_total, int64_t* passes) {
   if (!h || !ms_total || !passes) return PPCA_ERR_INVALID_ARG;
   cudaSetDevice(h->c.device);
   return pass_time_collect(&h->c, ms_total, passes);
+}
+
+ppca_status ppca_get_kernel_time(ppca_ctx* h, int which, double* ms_total, int64_t* launches) {
+  if (!h || !ms_total || !launches || which < 0 || which > 1) return PPCA_ERR_INVALID_ARG;
+  cudaSetDevice(h->c.device);
+  return kernel_time_collect(&h->c, which, ms_total, launches);
 }
 
 // (undocumented, profiling) per-role mbarrier wait cycles of the tensor-core kernel A since last call

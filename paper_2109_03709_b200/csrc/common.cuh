@@ -43,6 +43,9 @@ struct Ctx {
   bool timing = false;
   std::vector<cudaEvent_t> tev;
   size_t tev_used = 0;
+  // per-kernel timing of the tensor-core pass kernels: [0] kernel A (Y = XW'ᵀ, S), [1] kernel B (Zᵀ = XᵀY)
+  std::vector<cudaEvent_t> kev[2];
+  size_t kev_used[2] = {0, 0};
   std::string last_error;
   // grow-only scratch slots
   static const int kSlots = 24;

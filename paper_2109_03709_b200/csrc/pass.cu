@@ -95,6 +95,38 @@ ppca_status pass_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const 
   return pass_gram_impl(c, X, plan, W, m, S);
 }
 
+static cudaEvent_t kernel_event(Ctx* c, int which) {
+  auto& v = c->kev[which];
+  if (c->kev_used[which] == v.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    v.push_back(e);
+  }
+  return v[c->kev_used[which]++];
+}
+
+void kernel_timer_mark(Ctx* c, int which) {
+  if (c->timing) cudaEventRecord(kernel_event(c, which), c->stream);
+}
+
+ppca_status kernel_time_collect(Ctx* c, int which, double* ms, int64_t* n) {
+  cudaStreamSynchronize(c->stream);
+  double tot = 0.0;
+  int64_t cnt = 0;
+  for (size_t i = 0; i + 1 < c->kev_used[which]; i += 2) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->kev[which][i], c->kev[which][i + 1]) == cudaSuccess) {
+      tot += t;
+      ++cnt;
+    }
+  }
+  cudaGetLastError();
+  c->kev_used[which] = 0;
+  *ms = tot;
+  *n = cnt;
+  return PPCA_OK;
+}
+
 ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n) {
   cudaStreamSynchronize(c->stream);
   double tot = 0.0;
@@ -142,6 +174,11 @@ void pass_release(Ctx* c) {
   for (auto e : c->tev) cudaEventDestroy(e);
   c->tev.clear();
   c->tev_used = 0;
+  for (int w = 0; w < 2; ++w) {
+    for (auto e : c->kev[w]) cudaEventDestroy(e);
+    c->kev[w].clear();
+    c->kev_used[w] = 0;
+  }
 }
 
 }  // namespace ppca

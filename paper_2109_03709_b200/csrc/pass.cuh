@@ -20,6 +20,10 @@ ppca_status pass_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const
 ppca_status pass_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S);
 void pass_release(Ctx* c);
 ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n);
+// per-kernel CUDA events around the tensor-core kernels (which: 0 = kernel A, 1 = kernel B); a mark pair
+// brackets one launch
+void kernel_timer_mark(Ctx* c, int which);
+ppca_status kernel_time_collect(Ctx* c, int which, double* ms, int64_t* n);
 
 // building blocks (SIMT), local rows [r0, r0+rows)
 ppca_status xw(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* W, int m, float* Y);

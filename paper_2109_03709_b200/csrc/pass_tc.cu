@@ -324,9 +324,11 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * (smma ? 2 : 1) * mp * mp * sizeof(double));
   if (!Spart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   kp.Spart = Spart;
+  kernel_timer_mark(c, 0);
   PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka2<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
            : X->dtype == PPCA_F32_SPLIT ? dispatch_ka2<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
                                         : dispatch_ka<0>(c, mp, tmW, tmX, tmXlo, kp, grid));
+  kernel_timer_mark(c, 0);
   if (ksplit > 1) return PPCA_OK;                 // partial Y out; the caller forms S from the summed Y
   if (smma)
     reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
@@ -422,12 +424,14 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   // product 2 reads X_hi only: bf16 X, or the hi plane of a split X, by TMA
   if (X->dtype != PPCA_F32 && !make_x_maps(X, kb::KR, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   const int grid = (int)std::min<int64_t>(ctas, bp.ndg * bp.nrg);
+  kernel_timer_mark(c, 1);
   if (X->dtype == PPCA_F32)
     PPCA_TRY((dispatch_kb<false, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   else if (precise && X->dtype == PPCA_F32_SPLIT)
     PPCA_TRY((dispatch_kb<true, true>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   else
     PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
+  kernel_timer_mark(c, 1);
   reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
