@@ -165,6 +165,16 @@ ppca_status ppca_prime_eigengame(ppca_ctx* ctx, const ppca_matrix* X, int m, int
 ppca_status ppca_refine(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k,
                         float* E, double* theta_host, int* subspace_dim);
 
+/* Row-subsampled pPCA refinement (§5.2: "we only project 10% of the data for computing
+ * full-PCA"; reading R25): as ppca_refine, but the projected covariance
+ * is formed from the 128-row tiles of each shard whose Philox4x32-10 uniform (sample_seed, stream 7,
+ * key = global tile index for CONTIGUOUS shards) is below `fraction`, and θ are rescaled by
+ * n_global / rows used (an estimate of XᵀX's eigenvalues).  fraction ≥ 1 is ppca_refine.
+ * rows_used (optional): rows in the sample over all ranks.  An empty sample is INVALID_ARG. */
+ppca_status ppca_refine_sampled(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k,
+                                double fraction, uint64_t sample_seed, float* E, double* theta_host,
+                                int* subspace_dim, int64_t* rows_used);
+
 /* Evaluation (§5.3): angle_i = arccos(min(1,|<E_i,T_i>|)) and
  * LCES(V) = #consecutive i from 1 with angle_i < V (strict), for each threshold.
  * E, T: device [k][d] unit rows.  angles_host: double[k]; lces_host: int[nthr]. */

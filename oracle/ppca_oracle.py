@@ -279,6 +279,33 @@ def ppca_refine(X: np.ndarray, V: np.ndarray, k: int):
     return E, theta[:k], theta, B.shape[0]
 
 
+SAMPLE_TILE = 128          # rows per sampling unit (R25)
+STREAM_SAMPLE = 7          # Philox stream of the row-tile sample (R25)
+
+
+def sampled_rows(n: int, fraction: float, seed: int) -> np.ndarray:
+    """R25 (P L378 "we only project 10% of the data"): the row blocks [128t, 128t+128) ∩ [0, n) whose
+    uniform U(seed, stream 7, t) is below `fraction` (the random numbers are inputs: inputs.philox)."""
+    from inputs import philox as ph
+    nt = -(-n // SAMPLE_TILE)
+    u = ph.uniforms(seed, STREAM_SAMPLE, 0, nt)
+    keep = np.nonzero(u < fraction)[0]
+    if keep.size == 0:
+        return np.zeros(0, dtype=np.int64)
+    return np.concatenate([np.arange(t * SAMPLE_TILE, min(n, (t + 1) * SAMPLE_TILE)) for t in keep])
+
+
+def ppca_refine_sampled(X: np.ndarray, V: np.ndarray, k: int, fraction: float, seed: int):
+    """Row-subsampled pPCA (P L378): Alg. 1 with the projected covariance formed
+    from a seeded fraction of the rows and rescaled by n / rows used, so θ estimate XᵀX's eigenvalues
+    (the rescale leaves the eigenvectors unchanged).  Returns (E, θ[:k], rows used)."""
+    rows = sampled_rows(X.shape[0], fraction, seed) if fraction < 1.0 else np.arange(X.shape[0])
+    if rows.size == 0:
+        raise OracleError("empty row sample")
+    E, theta, _, _ = ppca_refine(X[rows], V, k)
+    return E, theta * (X.shape[0] / rows.size), rows.size
+
+
 def ritz_values(S: np.ndarray) -> np.ndarray:
     """Ritz values of an orthonormal-basis Gram S (the pPCA eigenvalue estimates)."""
     return jacobi_eigh(S)[0]

@@ -30,7 +30,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time"]
+           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled"]
 
 
 class PPCAError(RuntimeError):
@@ -90,6 +90,8 @@ def load(path: str = LIB_PATH):
         "ppca_last_pass_impl": (I, [P]),
         "ppca_get_pass_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "ppca_split_f32": (I, [P, P, I64, I64, I64]),
+        "ppca_refine_sampled": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, D, ctypes.c_uint64, P, P,
+                                    ctypes.POINTER(I), ctypes.POINTER(I64)]),
         "ppca_get_kernel_time": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
@@ -298,6 +300,18 @@ def ppca_refine(ctx, X: ppca_matrix, V, m: int, k: int, E) -> tuple[np.ndarray, 
     _check(ctx, load().ppca_refine(ctx, ctypes.byref(X), _ptr(V), m, k, _ptr(E), _np_ptr(theta),
                                    ctypes.byref(dim)), "ppca_refine")
     return theta, dim.value
+
+
+def ppca_refine_sampled(ctx, X: ppca_matrix, V, m: int, k: int, E, fraction: float,
+                        sample_seed: int) -> tuple[np.ndarray, int, int]:
+    """Row-subsampled refine: (θ rescaled to the full data, subspace dim, rows used)."""
+    theta = np.zeros(k, dtype=np.float64)
+    dim = ctypes.c_int()
+    used = ctypes.c_int64()
+    _check(ctx, load().ppca_refine_sampled(ctx, ctypes.byref(X), _ptr(V), m, k, fraction, sample_seed, _ptr(E),
+                                           _np_ptr(theta), ctypes.byref(dim), ctypes.byref(used)),
+           "ppca_refine_sampled")
+    return theta, dim.value, used.value
 
 
 def ppca_eval(ctx, E, T, k: int, d: int, thresholds) -> tuple[np.ndarray, np.ndarray]:

@@ -442,22 +442,49 @@ ppca_status ppca_prime_eigengame(ppca_ctx* h, const ppca_matrix* X, int m, int b
 }
 
 // ---------------------------------------------------------------------------- refine
-ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, float* E, double* theta_host,
-                        int* subspace_dim) {
-  if (!h) return PPCA_ERR_INVALID_ARG;
-  Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+// Alg. 1 steps 2-5 (P L47-51).  sample_fraction ≥ 1: all rows; otherwise only the 128-row tiles whose
+// Philox uniform (seed, stream 7, tile key) is < sample_fraction are projected (P L378 "we only project 10%
+// of the data"; reading R25) and θ are rescaled by n_global / rows used.
+static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int m, int k, double fraction,
+                               uint64_t sample_seed, float* E, double* theta_host, int* subspace_dim,
+                               int64_t* rows_used) {
   PPCA_TRY(check_matrix(c, X, m));
   if (!V || !E || k < 1 || k > m) return set_error(c, PPCA_ERR_INVALID_ARG, "bad refine args (k=%d, m=%d)", k, m);
+  if (!(fraction > 0.0)) return set_error(c, PPCA_ERR_INVALID_ARG, "sample fraction must be > 0");
   const int64_t d = X->d;
   float* B = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
-  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
-  double* S = (double*)scratch(c, S_S, (size_t)2 * m * m * sizeof(double));
+  double* S = (double*)scratch(c, S_S, (size_t)2 * m * m * sizeof(double) + 16);
   double* out = (double*)scratch(c, S_TC2, (size_t)m * sizeof(double) + (size_t)m * m * sizeof(double));
-  if (!B || !Y || !S || !out) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (!B || !S || !out) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   double* Bm = S + (size_t)m * m;
   double* theta_dev = out;
   double* R = out + m;
+  // row-tile sample (host: the Philox of common.cuh; the list is tiny — n_local/128 entries)
+  std::vector<int32_t> tiles;
+  double rows_local = (double)X->n_local;
+  const bool sampled = fraction < 1.0;
+  if (sampled) {
+    const int64_t tile = 128, nt = ceil_div(X->n_local, tile);
+    const int64_t r0 = X->layout == PPCA_LAYOUT_CONTIGUOUS ? c->rank * ceil_div(X->n_global, (int64_t)c->world) : 0;
+    rows_local = 0.0;
+    for (int64_t t = 0; t < nt; ++t) {
+      const uint64_t key = X->layout == PPCA_LAYOUT_CONTIGUOUS ? (uint64_t)((r0 + t * tile) / tile)
+                                                               : ((uint64_t)c->rank << 40) + (uint64_t)t;
+      if (u32_to_unit(philox_word(sample_seed, 7, key)) < fraction) {
+        tiles.push_back((int32_t)t);
+        rows_local += (double)(std::min(X->n_local, (t + 1) * tile) - t * tile);
+      }
+    }
+  }
+  double rows_total = rows_local;
+  if (c->world > 1) {
+    double* cnt = S + 2 * (size_t)m * m;
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(cnt, &rows_local, sizeof(double), cudaMemcpyHostToDevice, c->stream), "count"));
+    PPCA_TRY(allreduce(c, cnt, 1, true));
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(&rows_total, cnt, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "count"));
+    PPCA_TRY(check_cuda(c, cudaStreamSynchronize(c->stream), "count"));
+  }
+  if (sampled && rows_total <= 0.0) return set_error(c, PPCA_ERR_INVALID_ARG, "the row sample is empty");
   PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream), "copy V"));
   PPCA_TRY(normalize_rows(c, B, m, d));                 // current_components
   int mm = m;
@@ -470,17 +497,47 @@ ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m
   }
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, mm, &plan));
-  PPCA_TRY(pass_gram(c, X, &plan, B, mm, S));            // S = (XBᵀ)ᵀ(XBᵀ)
+  if (sampled) {
+    int32_t* td = (int32_t*)scratch(c, S_TILES, std::max<size_t>(1, tiles.size()) * sizeof(int32_t));
+    if (!td) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    if (!tiles.empty())
+      PPCA_TRY(check_cuda(c, cudaMemcpyAsync(td, tiles.data(), tiles.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                             c->stream), "copy tiles"));
+    plan.tiles_dev = td;
+    plan.tiles_host = tiles.data();
+    plan.ntiles_sel = (int64_t)tiles.size();
+  }
+  PPCA_TRY(pass_gram(c, X, &plan, B, mm, S));            // S = (XBᵀ)ᵀ(XBᵀ) over the (sampled) rows
   PPCA_TRY(allreduce(c, S, (size_t)mm * mm, true));
   const float* Bop = plan.Wop;                            // the operand rows the pass used
   PPCA_TRY(vec_gram(c, Bop, mm, d, Bm));
   PPCA_TRY(ritz_solve(c, S, Bm, mm, theta_dev, R, c->stream));
   PPCA_TRY(lift_rows(c, R, mm, Bop, mm, k, d, E, true, c->stream));
   PPCA_TRY(finish(c, "ppca_refine"));
-  if (theta_host && cudaMemcpy(theta_host, theta_dev, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return set_error(c, PPCA_ERR_CUDA, "copy theta");
+  if (theta_host) {
+    if (cudaMemcpy(theta_host, theta_dev, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return set_error(c, PPCA_ERR_CUDA, "copy theta");
+    if (sampled)
+      for (int i = 0; i < k; ++i) theta_host[i] *= (double)X->n_global / rows_total;
+  }
   if (subspace_dim) *subspace_dim = mm;
+  if (rows_used) *rows_used = (int64_t)rows_total;
   return PPCA_OK;
+}
+
+ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, float* E, double* theta_host,
+                        int* subspace_dim) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  cudaSetDevice(h->c.device);
+  return refine_impl(&h->c, X, V, m, k, 1.0, 0, E, theta_host, subspace_dim, nullptr);
+}
+
+ppca_status ppca_refine_sampled(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, double fraction,
+                                uint64_t sample_seed, float* E, double* theta_host, int* subspace_dim,
+                                int64_t* rows_used) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  cudaSetDevice(h->c.device);
+  return refine_impl(&h->c, X, V, m, k, fraction, sample_seed, E, theta_host, subspace_dim, rows_used);
 }
 
 // ---------------------------------------------------------------------------- eval / support

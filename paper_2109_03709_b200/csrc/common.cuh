@@ -48,7 +48,7 @@ struct Ctx {
   size_t kev_used[2] = {0, 0};
   std::string last_error;
   // grow-only scratch slots
-  static const int kSlots = 24;
+  static const int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_bytes[kSlots] = {};
 };
@@ -67,6 +67,7 @@ enum Slot {
   S_GEN0, S_GEN1, S_GEN2, S_GEN3,  // generator buffers
   S_EVAL,
   S_TC0, S_TC1, S_TC2, S_TC3, S_TC4,   // tensor-core pass scratch
+  S_TILES,                         // row-tile list of the subsampled refine (int32)
   S_NTSTAGE,
 };
 

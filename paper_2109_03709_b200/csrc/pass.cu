@@ -159,9 +159,36 @@ static ppca_status pass_power_impl(Ctx* c, const ppca_matrix* X, const PassPlan*
   return yty(c, Y, m, X->n_local, S);
 }
 
+__global__ void add_f64_kernel(double* __restrict__ acc, const double* __restrict__ v, int64_t count) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < count) acc[e] += v[e];
+}
+
 static ppca_status pass_gram_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
                                   double* S) {
-  if (plan->impl == 2) return pass_tc_gram(c, X, plan, W, m, S);
+  const bool sampled = plan->ntiles_sel >= 0;
+  // tensor-core pass (the tile list is read by kernel A2; the plain-fp32 converter kernel has none)
+  if (plan->impl == 2 && !(sampled && X->dtype == PPCA_F32)) return pass_tc_gram(c, X, plan, W, m, S);
+  if (sampled) {
+    // CUDA-core pass over runs of consecutive selected tiles, S summed over runs in a fixed order
+    const int64_t tile = 128;
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(S, 0, (size_t)m * m * sizeof(double), c->stream), "memset"));
+    double* Sr = (double*)scratch(c, S_GRAM, (size_t)m * m * sizeof(double));
+    float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
+    if (!Sr || !Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    for (int64_t i = 0; i < plan->ntiles_sel;) {
+      int64_t j = i + 1;
+      while (j < plan->ntiles_sel && plan->tiles_host[j] == plan->tiles_host[j - 1] + 1) ++j;
+      const int64_t r0 = plan->tiles_host[i] * tile;
+      const int64_t rows = std::min(X->n_local, plan->tiles_host[j - 1] * tile + tile) - r0;
+      PPCA_TRY(xw(c, X, r0, rows, W, m, Y));
+      PPCA_TRY(yty(c, Y, m, rows, Sr));
+      add_f64_kernel<<<(unsigned)ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(S, Sr, (int64_t)m * m);
+      PPCA_LAUNCH_CHECK(c, "add_f64");
+      i = j;
+    }
+    return PPCA_OK;
+  }
   float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
   if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   if (X->n_local == 0) return check_cuda(c, cudaMemsetAsync(S, 0, (size_t)m * m * sizeof(double), c->stream), "memset");

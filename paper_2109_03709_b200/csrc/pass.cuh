@@ -9,6 +9,10 @@ namespace ppca {
 struct PassPlan {
   int impl = 1;
   bool precise = false;         // product 2 also reads X_lo of a split X (minibatch steps: Q is the update)
+  // refine-mode pass over a subset of 128-row tiles (row-subsampled refine): device and host lists
+  const int32_t* tiles_dev = nullptr;
+  const int32_t* tiles_host = nullptr;
+  int64_t ntiles_sel = -1;      // < 0: all rows
   const float* Wop = nullptr;   // fp32 values of the operand rows the last pass actually used
                                 // (W itself for SIMT; RN_bf16(W) for tcgen05) — for the Ritz Gram
 };

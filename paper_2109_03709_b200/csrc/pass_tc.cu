@@ -301,14 +301,16 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
 }
 
 static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, int mp, double* S,
-                          __nv_bfloat16* YT, int64_t ldyt, int ksplit = 1, float* Ypart = nullptr) {
+                          __nv_bfloat16* YT, int64_t ldyt, int ksplit = 1, float* Ypart = nullptr,
+                          const int32_t* tiles = nullptr, int64_t ntiles_sel = -1) {
   CUtensorMap tmW, tmX, tmXlo;
   if (!make_map_bf16(&tmW, Wb, X->d, 2 * mp, X->d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
   tmX = tmXlo = tmW;   // unused unless X is staged by TMA
   if (X->dtype != PPCA_F32 && !make_x_maps(X, 128, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   KAParams kp;
   kp.X = X->data; kp.n = X->n_local; kp.d = X->d; kp.ld = X->ld; kp.m = m; kp.mp = mp;
-  kp.ntiles = ceil_div(X->n_local, ka::BM);
+  kp.ntiles = tiles ? ntiles_sel : ceil_div(X->n_local, ka::BM);
+  kp.tiles = tiles;
   kp.nk = ceil_div(X->d, ka::BK);
   kp.YT = YT; kp.ldyt = ldyt;
   kp.ksplit = ksplit;
@@ -317,7 +319,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   static int dbg = -1;
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   kp.dbg = dbg;
-  int grid = (int)std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit);
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit));
   // TMA-staged X (bf16, split) runs kernel A2; its S partial has 2·mp rows when S is on the tensor cores
   const bool tma_x = X->dtype != PPCA_F32;
   const bool smma = tma_x && mp == 64;
@@ -344,7 +346,7 @@ ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, con
   float* Wr;
   PPCA_TRY(prep_w(c, W, m, mp, X->d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
-  return run_ka(c, X, Wb, m, mp, S, nullptr, 0);
+  return run_ka(c, X, Wb, m, mp, S, nullptr, 0, 1, nullptr, plan->tiles_dev, plan->ntiles_sel);
 }
 
 // Y of a K-split row window: Y = Σ_parts Ypart (fixed order) → Yᵀ bf16 pair [2·mp][ldyt] (rows ≥ n zero)

@@ -52,6 +52,8 @@ struct KAParams {
   int ksplit = 1;
   int64_t kper = 0;       // K chunks per part
   float* Ypart = nullptr;
+  // row-tile list (kernel A2 only): item tiles are tiles[i] instead of i (the row-subsampled refine)
+  const int32_t* tiles = nullptr;
 };
 
 template <int MP, int XM>

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   const int64_t nitems = p.ntiles * p.ksplit, i0 = blockIdx.x, istep = gridDim.x;
   const bool partial = p.ksplit > 1;
   auto item = [&](int64_t it, int64_t& t, int64_t& k0, int64_t& k1, int64_t& nseg) {
-    t = it / p.ksplit;
+    t = p.tiles ? (int64_t)p.tiles[it / p.ksplit] : it / p.ksplit;
     k0 = (it % p.ksplit) * p.kper;
     k1 = min(p.nk, k0 + p.kper);
     nseg = k1 > k0 ? (k1 - k0 + KSEG - 1) / KSEG : 0;

@@ -259,6 +259,30 @@ def test_refine_parity_random_priming(P, ctx, name, impl, split):
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), name, th_all_ref)
 
 
+@pytest.mark.parametrize("impl", [1, 2], indirect=True, ids=["simt", "tcgen05"])
+@pytest.mark.parametrize("fraction", [0.1, 0.5])
+def test_refine_sampled_parity_c3s(P, ctx, impl, fraction):
+    """Row-subsampled refine (P L378, R25): the same seeded row tiles on both sides."""
+    import torch
+    w = C.SMALL["C3s"]
+    s = w.spec
+    Xs, X64 = _host(w)
+    lam, T = O.truth(X64)
+    rng = np.random.default_rng(17)
+    V32 = (T[: w.m] + 0.05 * rng.standard_normal((w.m, s.d)) / math.sqrt(s.d)).astype(np.float32)
+    E_ref, th_ref, used_ref = O.ppca_refine_sampled(X64, V32.astype(np.float64), w.k, fraction, 99)
+    Xm = _device_matrix(P, ctx, Xs, s, impl == 2)
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    th, dim, used = P.ppca_refine_sampled(ctx, Xm, torch.from_numpy(V32).cuda(), w.m, w.k, E, fraction, 99)
+    assert used == used_ref and dim == w.m
+    assert P.ppca_last_pass_impl(ctx) == impl
+    err = U.ritz_rel_err(th, th_ref)
+    print(f"\n[parity] C3s sampled refine f={fraction} impl={impl}: rows {used}, Ritz rel err {err:.3e}")
+    assert err < 1e-4
+    gi = U.gapped(th_ref, w.k)
+    assert U.abs_cos(E.cpu().numpy()[gi], E_ref[gi]).min() >= 0.9999
+
+
 # ----------------------------------------------------------------------------- refine edge cases
 def test_refine_counterexample_on_gpu(P, ctx):
     """§4.1 (P L195–228) through the C ABI: d = 3 (row stride padded to 4)."""

@@ -324,3 +324,32 @@ def test_theorem1_mechanism_near_converged():
 def test_relative_gaps():
     g = O.relative_gaps(np.array([10.0, 5.0, 4.0, 1.0]))
     np.testing.assert_allclose(g, [0.5, 0.2, 0.25, 3.0])
+
+
+# ----------------------------------------------------------------------------- row-subsampled refine (R25)
+def test_sampled_refine_reduces_to_refine_and_is_unbiased():
+    X = _random_data(3000, 10, 21)
+    rng = np.random.default_rng(22)
+    V = rng.standard_normal((6, 10))
+    # fraction 1 is the plain refine
+    E1, th1, used = O.ppca_refine_sampled(X, V, 3, 1.0, 5)
+    E0, th0, _, _ = O.ppca_refine(X, V, 3)
+    assert used == 3000
+    np.testing.assert_allclose(th1, th0, rtol=1e-13)
+    np.testing.assert_allclose(E1, E0, atol=1e-12)
+    # the sample is whole 128-row tiles, deterministic in the seed, about `fraction` of them
+    rows = O.sampled_rows(100_000, 0.1, 7)
+    cnt = np.bincount(rows // 128, minlength=782)          # 100000 rows = 781 full tiles + 32
+    assert np.all(np.isin(cnt[:-1], [0, 128])) and cnt[-1] in (0, 32)
+    np.testing.assert_array_equal(rows, O.sampled_rows(100_000, 0.1, 7))
+    assert abs(rows.size / 100_000 - 0.1) < 0.02
+    # the rescaled projected covariance is an unbiased estimate: mean over seeds ≈ the full one
+    B = O.gram_schmidt(V)
+    S_full = O.projected_gram(X, B)
+    acc = np.zeros_like(S_full)
+    seeds = range(40)
+    for sd in seeds:
+        r = O.sampled_rows(3000, 0.5, sd)
+        acc += O.projected_gram(X[r], B) * (3000 / r.size)
+    acc /= len(seeds)
+    assert np.linalg.norm(acc - S_full) / np.linalg.norm(S_full) < 0.05
