@@ -206,7 +206,8 @@ ppca_status ppca_get_pass_time(ppca_ctx* ctx, double* ms_total, int64_t* passes)
  * CUDA events on the context stream; returns the summed device time (ms) and launch count, then resets. */
 ppca_status ppca_get_kernel_time(ppca_ctx* ctx, int which, double* ms_total, int64_t* launches);
 
-/* Timing hook: select the fused-pass implementation (0 = auto, 1 = SIMT fp32, 2 = tcgen05).
+/* Timing hook: select the fused-pass implementation (0 = auto, 1 = SIMT fp32, 2 = tcgen05, 3 = tcgen05
+ * with the power pass as two kernels instead of the single-read fused kernel; 3 reports as 2).
  * Returns UNSUPPORTED if the requested path cannot run this matrix. */
 ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);
 /* Implementation used by the most recent pass (1 = SIMT, 2 = tcgen05; 0 = none yet). */

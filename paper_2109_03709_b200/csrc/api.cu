@@ -228,6 +228,7 @@ ppca_status ppca_ctx_destroy(ppca_ctx* h) {
   for (int i = 0; i < Ctx::kSlots; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
   if (c->d_err) cudaFree(c->d_err);
+  if (c->flags) cudaFree(c->flags);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->side) cudaStreamDestroy(c->side);
@@ -271,7 +272,7 @@ ppca_status ppca_debug_wait_counters(unsigned long long* out16) { return ppca::d
 int ppca_last_pass_impl(const ppca_ctx* h) { return h ? h->c.last_impl : -1; }
 
 ppca_status ppca_set_pass_impl(ppca_ctx* h, int impl) {
-  if (!h || impl < 0 || impl > 2) return PPCA_ERR_INVALID_ARG;
+  if (!h || impl < 0 || impl > 3) return PPCA_ERR_INVALID_ARG;
   h->c.pass_impl = impl;
   return PPCA_OK;
 }

@@ -35,7 +35,10 @@ struct Ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   void* nccl_comm = nullptr;          // ncclComm_t when world > 1
   int* d_err = nullptr;               // device error word
-  int pass_impl = 0;                  // 0 auto, 1 simt, 2 tcgen05
+  int pass_impl = 0;                  // 0 auto, 1 simt, 2 tcgen05, 3 tcgen05 without the fused power pass
+  int* flags = nullptr;               // per-tile ready flags of the fused power pass (device, zeroed)
+  int64_t flags_n = 0;
+  int epoch = 0;
   int last_impl = 0;                  // implementation of the most recent pass
   int sm_count = 148;
   int64_t launches = 0;

@@ -52,7 +52,7 @@ ppca_status pass_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan) {
   if (c->pass_impl == 0 && X->n_local * X->d < (int64_t(1) << 24)) return PPCA_OK;
   ppca_status s = pass_tc_prepare(c, X, m, plan);
   if (s == PPCA_OK) return PPCA_OK;
-  if (c->pass_impl == 2) return s;         // explicitly requested: report why it cannot run
+  if (c->pass_impl >= 2) return s;         // explicitly requested: report why it cannot run
   plan->impl = 1;                          // auto: shapes the tensor-core pass does not cover
   return PPCA_OK;
 }

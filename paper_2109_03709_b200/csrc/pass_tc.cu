@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
   }
 }
 
+// ============================================================================ fused power pass (tc_fused.cuh)
+#include "tc_fused.cuh"
+
 // ============================================================================ kernel B (tc_xty.cuh)
 #include "tc_xty.cuh"
 
@@ -377,6 +380,114 @@ static int pick_ksplit(const Ctx* c, const ppca_matrix* X, int64_t nk) {
   return (int)ceil_div(nk, kper);
 }
 
+template <int XM, int NSTA, int NWS, int NSTB>
+static constexpr size_t fused_smem() {
+  return 1024 + (size_t)NSTA * (XM == 2 ? 2 * kf::XPL : kf::XPL) + (size_t)NWS * kf::WST +
+         (size_t)NSTB * (kf::BX + kf::BY) + 256;
+}
+
+template <int XM, int NSTA, int NWS, int NSTB>
+static void launch_fused(Ctx* c, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
+                         const CUtensorMap& tmXb, const CUtensorMap& tmY, const KFParams& fp) {
+  constexpr size_t smem = fused_smem<XM, NSTA, NWS, NSTB>();
+  static_assert(smem <= 227 * 1024, "fused kernel shared memory budget");
+  auto kern = xwz_fused_kernel<XM, NSTA, NWS, NSTB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, kf::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, tmXb, tmY, fp);
+}
+
+template <int XM>
+static void launch_fused_cfg(Ctx* c, int cfg, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                             const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const CUtensorMap& tmY,
+                             const KFParams& fp) {
+  // (X stages, W' stages, B stages): the L2-fed B-stream is the limiter, so it gets the deepest ring
+  // (measured on C3: (2,2,5) 0.99 ms, (3,2,4) 1.05, (3,3,3) 1.09, (4,3,2) 1.15); PPCA_FUSED_CFG selects others
+  switch (cfg) {
+    case 1: launch_fused<XM, 4, 3, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 2: launch_fused<XM, 3, 2, 4>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 3: launch_fused<XM, 3, 3, 3>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 4: launch_fused<XM, 2, 1, 6>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    default: launch_fused<XM, 2, 2, 5>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+  }
+}
+
+// The single-read power pass: TMA-staged X (bf16 / split), m ≤ 64 (padded to 64), d ≤ KSEG·BK (one
+// accumulation segment), a whole row tile per CTA at least.
+static bool fused_eligible(const Ctx* c, const ppca_matrix* X, int mp, bool precise) {
+  return c->pass_impl != 3 && !precise && X->dtype != PPCA_F32 && mp == 64 && X->d <= ka2::KSEG * ka2::BK &&
+         X->n_local >= 128;
+}
+
+static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, float* Z,
+                                    double* S) {
+  const int mp = 64;
+  const int64_t n = X->n_local, d = X->d;
+  const int64_t ntiles = ceil_div(n, kf::BM);
+  const int64_t ctas = persistent_ctas(c);
+  const int ndg = (int)ceil_div(d, (int64_t)kf::DG);
+  int nrg = (int)std::max<int64_t>(1, std::min<int64_t>(ctas / ndg, ntiles));
+  const int64_t tpr = ceil_div(ntiles, (int64_t)nrg);
+  nrg = (int)ceil_div(ntiles, tpr);
+  const int grid = ndg * nrg;
+  const int64_t nrow_pad = ntiles * kf::BM;
+  __nv_bfloat16* Yrm = (__nv_bfloat16*)scratch(c, S_Y, (size_t)nrow_pad * 2 * mp * 2);
+  double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * 2 * mp * mp * sizeof(double));
+  const int64_t dpad = (int64_t)ndg * kf::DG;
+  float* Zp = (float*)scratch(c, S_PART, (size_t)nrg * dpad * mp * sizeof(float));
+  if (!Yrm || !Spart || !Zp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (c->flags_n < ntiles) {                     // per-tile ready flags: zeroed once, epochs count up
+    if (c->flags) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(c->flags);
+      c->flags = nullptr;
+    }
+    if (cudaMalloc(&c->flags, (size_t)ntiles * sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      c->flags_n = 0;
+      return set_error(c, PPCA_ERR_CUDA, "flags alloc failed");
+    }
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(c->flags, 0, (size_t)ntiles * sizeof(int), c->stream), "flags"));
+    c->flags_n = ntiles;
+    c->epoch = 0;
+  }
+  if (++c->epoch >= (1 << 30)) {
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(c->flags, 0, (size_t)c->flags_n * sizeof(int), c->stream), "flags"));
+    c->epoch = 1;
+  }
+  CUtensorMap tmW, tmX, tmXlo, tmXb, tmXblo, tmY;
+  if (!make_map_bf16(&tmW, Wb, d, 2 * mp, d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
+  tmXlo = tmW;
+  if (!make_x_maps(X, kf::BM, &tmX, &tmXlo) || !make_x_maps(X, kf::KR, &tmXb, &tmXblo))
+    return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
+  if (!make_map_bf16(&tmY, Yrm, 2 * mp, nrow_pad, 2 * mp, kf::KR)) return set_error(c, PPCA_ERR_CUDA, "tensor map Y failed");
+  KFParams fp;
+  fp.n = n; fp.d = d; fp.m = m;
+  fp.ntiles = ntiles; fp.nk = ceil_div(d, (int64_t)kf::BK); fp.nseg = 1;
+  fp.ndg = ndg; fp.nrg = nrg; fp.tiles_per_rg = tpr;
+  fp.Yrm = Yrm; fp.nrow_pad = nrow_pad; fp.Spart = Spart; fp.Zp = Zp;
+  fp.flags = c->flags; fp.epoch = c->epoch;
+  static int pf = -1;
+  if (pf < 0) pf = getenv("PPCA_FUSED_PF") ? atoi(getenv("PPCA_FUSED_PF")) : 0;
+  fp.pf = pf;
+  static int dbg = -1;
+  if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
+  fp.dbg = dbg;
+  kernel_timer_mark(c, 0);
+  static int cfg = -1;
+  if (cfg < 0) cfg = getenv("PPCA_FUSED_CFG") ? atoi(getenv("PPCA_FUSED_CFG")) : 0;
+  if (X->dtype == PPCA_F32_SPLIT)
+    launch_fused_cfg<2>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+  else
+    launch_fused_cfg<1>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+  PPCA_LAUNCH_CHECK(c, "xwz_fused_kernel");
+  kernel_timer_mark(c, 0);
+  reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+  PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+  PPCA_LAUNCH_CHECK(c, "reduce_zp");
+  return PPCA_OK;
+}
+
 ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, float* Z, double* S,
                           bool precise) {
   const int mp = pad16(m);
@@ -385,6 +496,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   float* Wr;
   PPCA_TRY(prep_w(c, W, m, mp, d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
+  if (fused_eligible(c, X, mp, precise)) return pass_fused_power(c, X, Wb, m, Z, S);
   // Yᵀ as a bf16 pair [Y_hi; Y_lo], [2·mp][ldyt]; kernel A writes every row and column < ldyt
   const int64_t ldyt = ceil_div(n, 64) * 64;
   __nv_bfloat16* YT = (__nv_bfloat16*)scratch(c, S_Y, (size_t)2 * mp * ldyt * 2);

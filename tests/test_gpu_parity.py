@@ -141,11 +141,13 @@ def _device_matrix(P, ctx, Xs, spec, split):
 
 
 @pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
-@pytest.mark.parametrize("impl", [1, 2], indirect=True, ids=["simt", "tcgen05"])
+@pytest.mark.parametrize("impl", [1, 2, 3], indirect=True, ids=["simt", "tcgen05", "tcgen05-2kernel"])
 @pytest.mark.parametrize("name", ["C1", "C3s", "C5s"])
 def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
+    """impl 2 runs the single-read fused power pass where eligible (split/bf16 X, m ≤ 64, d ≤ 1024: C3s
+    split); impl 3 forces the two-kernel pass."""
     import torch
-    if impl == 2 and name == "C1":
+    if impl >= 2 and name == "C1":
         pytest.skip("auto keeps 0.5 MB shards on the fp32 SIMT pass (bf16 rounding of X at n=2000 ~1e-4)")
     w = C.SMALL[name]
     s = w.spec
@@ -160,7 +162,7 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
     Xm = _device_matrix(P, ctx, Xs, s, split)
     W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
     th_hist = P.ppca_prime_power(ctx, Xm, w.m, w.iters, w.init_seed, W, theta_hist=True)
-    assert P.ppca_last_pass_impl(ctx) == impl
+    assert P.ppca_last_pass_impl(ctx) == min(impl, 2)
     Wh = W.cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(Wh @ Wh.T, np.eye(w.m), atol=5e-6)
     # the primed subspace equals the oracle's (largest principal angle)
