@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
           if (p.pf) prefetch();
           mbar_wait(&aempty[s], ph ^ 1);
           mbar_arrive_expect_tx(&afull[s], XSTG);
-          tma_load_2d_hint(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM), keep);
+          if (p.dbg & 2)
+            tma_load_2d(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM));
+          else
+            tma_load_2d_hint(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM), keep);
           if (LO) tma_load_2d_hint(sA + s * XSTG + XPL, &tmXlo, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM), drop);
         }
       }
