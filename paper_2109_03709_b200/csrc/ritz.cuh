@@ -115,9 +115,10 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
         csn[2 * i + 1] = ss;
       }
       __syncthreads();
-      // A ← JᵀAJ one (pair a, pair b) 2×2 block at a time; V ← VJ one (row, pair) couple at a time
-      for (int e = tid; e < np * np; e += nt) {
-        const int ia = e / np, ib = e % np;
+      // A ← JᵀAJ one (pair a, pair b) 2×2 block at a time; V ← VJ one (row, pair) couple at a time.
+      // Index maps without per-element integer division: thread → (ia, ib) = (tid / np + k·nt/np, tid % np)
+      // when np divides nt (m a power of two), else the general e / np map.
+      auto block = [&](int ia, int ib) {
         const int p = pq[2 * ia], q = pq[2 * ia + 1], p2 = pq[2 * ib], q2 = pq[2 * ib + 1];
         const double c1 = csn[2 * ia], s1 = csn[2 * ia + 1], c2 = csn[2 * ib], s2 = csn[2 * ib + 1];
         const double a = A[p * mm + p2], b = A[p * mm + q2], c = A[q * mm + p2], d = A[q * mm + q2];
@@ -127,14 +128,25 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
         A[p * mm + q2] = s2 * ra + c2 * rb;
         A[q * mm + p2] = c2 * rc - s2 * rd;
         A[q * mm + q2] = s2 * rc + c2 * rd;
-      }
-      for (int e = tid; e < (vectors ? np * mm : 0); e += nt) {   // V stored transposed: V[col·mm + row]
-        const int ia = e / mm, row = e % mm;
+      };
+      auto vrot = [&](int ia, int row) {                 // V stored transposed: V[col·mm + row]
         const int p = pq[2 * ia], q = pq[2 * ia + 1];
         const double cc = csn[2 * ia], ss = csn[2 * ia + 1];
         const double vp = (double)V[p * mm + row], vq = (double)V[q * mm + row];
         V[p * mm + row] = (VT)(cc * vp - ss * vq);
         V[q * mm + row] = (VT)(ss * vp + cc * vq);
+      };
+      if (nt % np == 0) {
+        for (int ia = tid / np; ia < np; ia += nt / np) block(ia, tid % np);
+      } else {
+        for (int e = tid; e < np * np; e += nt) block(e / np, e % np);
+      }
+      if (vectors) {
+        if (nt % mm == 0) {
+          for (int ia = tid / mm; ia < np; ia += nt / mm) vrot(ia, tid % mm);
+        } else {
+          for (int e = tid; e < np * mm; e += nt) vrot(e / mm, e % mm);
+        }
       }
       __syncthreads();
     }

@@ -56,71 +56,119 @@ ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G) {
 // ============================================================================ Cholesky (one CTA)
 // In smem A[m][m] (fp64).  Right-looking; pivots ≤ drop²·G_jj are dropped (column zeroed) if
 // drop > 0, else flag COLLAPSE.  Writes Linv (lower, dropped rows zero) and keep[] flags.
+// Blocked right-looking Cholesky in shared memory A[m][m] (fp64, lower, in place), column blocks of CB:
+// (1) the diagonal block by one warp (__syncwarp only), (2) the panel below by forward substitution, one
+// thread per row, (3) the trailing lower triangle from a transposed copy of the panel (conflict-free).
+// Pivots ≤ drop²·G_jj are dropped (column zeroed, keep[j] = 0) when drop > 0, else flag COLLAPSE.
+// About 3·m/CB block barriers instead of 2·m column barriers.
+constexpr int CB = 16;
 __device__ void block_cholesky(double* A, int m, double drop, int* keep, double* diag0, int* d_err) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double rdiag[PPCA_MAX_M];
+  __shared__ double panelT[CB][PPCA_MAX_M];
   for (int i = tid; i < m; i += nt) diag0[i] = A[i * m + i];
   __syncthreads();
-  __shared__ double colj[PPCA_MAX_M];    // scaled column j of L (row-contiguous copy)
-  for (int j = 0; j < m; ++j) {
-    // phase 1: every thread derives the pivot decision from A[j][j] (no broadcast barrier needed)
-    const double p = A[j * m + j];
-    const bool dr = drop > 0.0 ? !(p > drop * drop * diag0[j]) : (!(p > 0.0) || !isfinite(p));
-    if (tid == 0) {
-      keep[j] = !dr;
-      if (dr && drop <= 0.0) atomicOr(d_err, DEV_COLLAPSE);
-    }
-    if (dr) {
-      for (int i = j + tid; i < m; i += nt) colj[i] = 0.0;
-    } else {
-      const double piv = sqrt(p), rp = 1.0 / piv;
-      for (int i = j + tid; i < m; i += nt) colj[i] = (i == j) ? piv : A[i * m + j] * rp;
+  for (int kb = 0; kb < m; kb += CB) {
+    const int nb = min(CB, m - kb), ke = kb + nb;
+    if (warp == 0) {                              // (1) diagonal block
+      for (int j = kb; j < ke; ++j) {
+        const double p = A[j * m + j];
+        const bool dr = drop > 0.0 ? !(p > drop * drop * diag0[j]) : (!(p > 0.0) || !isfinite(p));
+        const double piv = dr ? 0.0 : sqrt(p), rp = dr ? 0.0 : 1.0 / piv;
+        const int i = j + 1 + lane;
+        const double lij = i < ke ? A[i * m + j] * rp : 0.0;
+        __syncwarp();
+        if (lane == 0) {
+          A[j * m + j] = piv;
+          keep[j] = !dr;
+          rdiag[j] = rp;
+          if (dr && drop <= 0.0) atomicOr(d_err, DEV_COLLAPSE);
+        }
+        if (i < ke) A[i * m + j] = lij;
+        __syncwarp();
+        // trailing part of the diagonal block: lane ↔ row ii = j+1+lane, columns (j, ii]; l_kk by shuffle
+        for (int kk = j + 1; kk < ke; ++kk) {
+          const double lk = __shfl_sync(0xffffffffu, lij, kk - j - 1);
+          if (i < ke && kk <= i) A[i * m + kk] -= lij * lk;
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
-    // phase 2: write column j, update the trailing lower triangle A[i][k] -= l_i l_k (k ≤ i)
-    for (int i = j + tid; i < m; i += nt) A[i * m + j] = colj[i];
-    if (!dr) {
-      // 2-D thread map (no integer division in the loop): rows i ≡ ty, columns k ≡ tx (mod 16), k ≤ i
+    for (int i = ke + tid; i < m; i += nt) {     // (2) panel rows: L11 x = a_i
+      double x[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        double sum = 0.0;
+        if (c < nb) {
+          sum = A[i * m + kb + c];
+#pragma unroll
+          for (int l = 0; l < c; ++l) sum -= x[l] * A[(kb + c) * m + kb + l];
+          sum *= rdiag[kb + c];
+          A[i * m + kb + c] = sum;
+          panelT[c][i] = sum;
+        }
+        x[c] = sum;
+      }
+    }
+    __syncthreads();
+    {                                             // (3) trailing lower triangle
       const int ty = tid >> 4, tx = tid & 15, sy = nt >> 4;
-      for (int i = j + 1 + ty; i < m; i += sy) {
-        const double li = colj[i];
-        double* Ai = A + i * m;
-        for (int k = j + 1 + tx; k <= i; k += 16) Ai[k] -= li * colj[k];
+      for (int i = ke + ty; i < m; i += sy) {
+        double li[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) li[c] = c < nb ? A[i * m + kb + c] : 0.0;
+        for (int k = ke + tx; k <= i; k += 16) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) acc = fma(li[c], c < nb ? panelT[c][k] : 0.0, acc);
+          A[i * m + k] -= acc;
+        }
       }
     }
     __syncthreads();
   }
 }
 
-// Linv = L⁻¹ (rows of dropped pivots zero), rows in order; for each row all columns cc ≤ i at once, with
-// blockDim/m threads per column splitting Σ_{cc≤j<i} L[i][j]·Linv[j][cc] (reduced in fixed order).
+// Linv = L⁻¹ (rows of dropped pivots zero) by row blocks of CB: T = Σ_{k < r0} L[r][k]·Linv[k][c] for the
+// block's rows and earlier columns (all threads), then a CB-row forward substitution per column (one thread
+// per column) with the block's diagonal reciprocals.  2 barriers per row block.
 __device__ void block_lower_inverse(const double* L, int m, const int* keep, double* Linv) {
-  __shared__ double red[512];
+  __shared__ double rd[PPCA_MAX_M];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int gpc = max(1, min(nt, 512) / m);
-  const int cc = tid % m, q = tid / m;
-  for (int i = 0; i < m; ++i) {
-    double part = 0.0;
-    if (q < gpc && cc < i && keep[i]) {
-      double p2 = 0.0;                         // two chains: half the dependent-FMA latency
-      int j = cc + q;
-      for (; j + gpc < i; j += 2 * gpc) {
-        part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
-        p2 = fma(L[i * m + j + gpc], Linv[(int64_t)(j + gpc) * m + cc], p2);
+  for (int i = tid; i < m; i += nt) rd[i] = (keep[i] && L[i * m + i] != 0.0) ? 1.0 / L[i * m + i] : 0.0;
+  __syncthreads();
+  for (int r0 = 0; r0 < m; r0 += CB) {
+    const int nb = min(CB, m - r0);
+    for (int e = tid; e < nb * r0; e += nt) {    // T into Linv[r][c], c < r0
+      const int r = r0 + e / r0, c = e % r0;
+      double a0 = 0.0, a1 = 0.0;
+      int k = c;
+      for (; k + 1 < r0; k += 2) {
+        a0 = fma(L[r * m + k], Linv[(int64_t)k * m + c], a0);
+        a1 = fma(L[r * m + k + 1], Linv[(int64_t)(k + 1) * m + c], a1);
       }
-      if (j < i) part = fma(L[i * m + j], Linv[(int64_t)j * m + cc], part);
-      part += p2;
+      if (k < r0) a0 = fma(L[r * m + k], Linv[(int64_t)k * m + c], a0);
+      Linv[(int64_t)r * m + c] = a0 + a1;
     }
-    if (q < gpc) red[q * m + cc] = part;
     __syncthreads();
-    for (int c2 = tid; c2 < m; c2 += nt) {
-      double v = 0.0;
-      if (keep[i] && c2 <= i) {
-        double sum = 0.0;
-        for (int q2 = 0; q2 < gpc; ++q2) sum += red[q2 * m + c2];
-        v = ((i == c2) ? 1.0 : 0.0) - sum;
-        v /= L[i * m + i];
+    for (int c = tid; c < m; c += nt) {           // forward substitution within the row block
+      double x[CB];
+#pragma unroll
+      for (int rr = 0; rr < CB; ++rr) {
+        double v = 0.0;
+        if (rr < nb) {
+          const int r = r0 + rr;
+          if (c <= r) {
+            double rhs = c < r0 ? -Linv[(int64_t)r * m + c] : (r == c ? 1.0 : 0.0);
+#pragma unroll
+            for (int l = 0; l < rr; ++l) rhs -= L[r * m + r0 + l] * x[l];
+            v = rhs * rd[r];
+          }
+          Linv[(int64_t)r * m + c] = v;
+        }
+        x[rr] = v;
       }
-      Linv[(int64_t)i * m + c2] = v;
     }
     __syncthreads();
   }
