@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
   for (int e = tid; e < m * m; e += nt) {            // lanes vary i: Linv[j][·] is a broadcast
     const int j = e / m, i = e % m;
     double s = 0.0;
-    for (int t = 0; t <= j; ++t) s += S[i * m + t] * Linv[j * m + t];
+    for (int t = 0; t <= j; ++t) s += S[t * m + i] * Linv[j * m + t];   // S symmetric: coalesced over i
     T1[i * m + j] = s;
   }
   __syncthreads();
@@ -171,6 +171,163 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
     R[e] = s;
   }
 }
+
+// Eigenvalues only (the per-iterate θ history of power priming, off the critical path but one per
+// iteration): C = L⁻¹SL⁻ᵀ as above, Householder tridiagonalisation of C (4 barriers per column), then all m
+// eigenvalues of the tridiagonal by Sturm-count multisection (nt/m threads per eigenvalue, 5 sub-intervals
+// per round).  O(m³/nt + m²) instead of Jacobi's O(sweeps·m) barrier rounds.
+__global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
+                                                          int m, double* __restrict__ gLinv, double* __restrict__ gT1,
+                                                          double* __restrict__ theta, int* d_err) {
+  extern __shared__ double sm[];
+  const bool small = m <= 64;
+  double* A = sm;                                     // m × m (C, then the reduced matrix)
+  double* Linv = small ? A + m * m : gLinv;
+  double* T1 = small ? A + 2 * m * m : gT1;
+  __shared__ double diag0[PPCA_MAX_M], vec[PPCA_MAX_M], pv[PPCA_MAX_M], ta[PPCA_MAX_M], tb[PPCA_MAX_M];
+  __shared__ int keep[PPCA_MAX_M];
+  __shared__ double sh_alpha, sh_beta, sh_k;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+
+  // 1. L = chol(B), L⁻¹, C = L⁻¹ S L⁻ᵀ (symmetrised)
+  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
+  __syncthreads();
+  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err);
+  ppca::block_lower_inverse(A, m, keep, Linv);
+  for (int e = tid; e < m * m; e += nt) {
+    const int j = e / m, i = e % m;
+    double s = 0.0;
+    for (int t = 0; t <= j; ++t) s += S[t * m + i] * Linv[j * m + t];   // S symmetric: coalesced over i
+    T1[i * m + j] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    double s = 0.0;
+    for (int t = 0; t <= i; ++t) s += Linv[i * m + t] * T1[t * m + j];
+    A[e] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    if (i < j) {
+      const double v = 0.5 * (A[i * m + j] + A[j * m + i]);
+      A[i * m + j] = v;
+      A[j * m + i] = v;
+    }
+  }
+  __syncthreads();
+  // 2. Householder tridiagonalisation (full symmetric matrix kept up to date)
+  for (int k = 0; k + 2 < m; ++k) {
+    const int n1 = m - k - 1;
+    const double* col = A + (k + 1) * m + k;          // x_i = A[k+1+i][k] (stride m)
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = lane; i < n1; i += 32) ss += col[i * m] * col[i * m];
+      ss = ppca::warp_sum(ss);
+      if (lane == 0) {
+        const double x0 = col[0];
+        const double alpha = ss > 0.0 ? -copysign(sqrt(ss), x0) : 0.0;
+        const double v0 = x0 - alpha;
+        const double vtv = ss - x0 * x0 + v0 * v0;
+        sh_alpha = alpha;
+        sh_beta = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        ta[k] = A[k * m + k];
+        tb[k] = alpha;
+      }
+    }
+    __syncthreads();
+    const double beta = sh_beta;
+    for (int i = tid; i < n1; i += nt) vec[i] = i == 0 ? col[0] - sh_alpha : col[i * m];
+    __syncthreads();
+    if (beta != 0.0) {
+      // p = β C' v, C' = A[k+1.., k+1..]: G threads per row (consecutive lanes), shuffle-reduced
+      // (uniform trip counts per warp: every lane reaches the shuffles)
+      const int G = nt / n1 >= 4 ? 4 : (nt / n1 >= 2 ? 2 : 1);
+      for (int b0 = 0; b0 < n1; b0 += nt / G) {
+        const int base = b0 + tid / G, q = tid % G;
+        const bool act = base < n1;
+        double acc = 0.0;
+        if (act) {
+          const double* row = A + (k + 1 + base) * m + (k + 1);
+          for (int j = q; j < n1; j += G) acc = fma(row[j], vec[j], acc);
+        }
+        for (int o = G / 2; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o, G);
+        if (act && q == 0) pv[base] = beta * acc;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double kk = 0.0;
+        for (int i = lane; i < n1; i += 32) kk += vec[i] * pv[i];
+        kk = ppca::warp_sum(kk);
+        if (lane == 0) sh_k = 0.5 * beta * kk;
+      }
+      __syncthreads();
+      for (int i = tid; i < n1; i += nt) pv[i] -= sh_k * vec[i];   // w = p − K v
+      __syncthreads();
+      // C' −= v wᵀ + w vᵀ  (2-D thread map: no integer division per element)
+      {
+        const int ty = tid >> 5, tx = tid & 31, sy = nt >> 5;
+        for (int i = ty; i < n1; i += sy) {
+          const double vi = vec[i], wi = pv[i];
+          double* Ai = A + (k + 1 + i) * m + (k + 1);
+          for (int j = tx; j < n1; j += 32) Ai[j] -= vi * pv[j] + wi * vec[j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (m >= 2) {
+      ta[m - 2] = A[(m - 2) * m + (m - 2)];
+      tb[m - 2] = A[(m - 1) * m + (m - 2)];
+    }
+    ta[m - 1] = A[(m - 1) * m + (m - 1)];
+  }
+  __syncthreads();
+  // 3. Sturm multisection: eigenvalue j (ascending) by G = nt/m threads; count(x) = #{i : d_i < 0}
+  double lo = 0.0, hi = 0.0;
+  for (int i = 0; i < m; ++i) {                        // Gershgorin bounds (every thread)
+    const double r = (i > 0 ? fabs(tb[i - 1]) : 0.0) + (i + 1 < m ? fabs(tb[i]) : 0.0);
+    lo = i == 0 ? ta[i] - r : fmin(lo, ta[i] - r);
+    hi = i == 0 ? ta[i] + r : fmax(hi, ta[i] + r);
+  }
+  const double span = fmax(hi - lo, 1e-300);
+  lo -= 1e-12 * span;
+  hi += 1e-12 * span;
+  // θ history needs ~1e-10 relative (the parity bar is 1e-4): (G+1)^rounds ≥ 2^42 of the Gershgorin span
+  const int G = nt / m >= 8 ? 8 : (nt / m >= 4 ? 4 : (nt / m >= 2 ? 2 : 1));
+  const int rounds = G == 8 ? 14 : (G == 4 ? 19 : (G == 2 ? 27 : 42));
+  for (int b0 = 0; b0 < m; b0 += nt / G) {              // uniform trip counts: every lane reaches the shuffles
+    const int q = tid % G, j = b0 + tid / G;
+    const bool act = j < m;
+    double L = lo, U = hi;
+    for (int round = 0; round < rounds; ++round) {
+      const double x = L + (U - L) * (double)(q + 1) / (double)(G + 1);
+      int cnt = 0;
+      double dd = 1.0;
+      for (int i = 0; i < (act ? m : 0); ++i) {
+        const double bs = i > 0 ? tb[i - 1] * tb[i - 1] : 0.0;
+        dd = (ta[i] - x) - (i > 0 ? bs / dd : 0.0);
+        if (dd == 0.0) dd = -1e-300;
+        cnt += dd < 0.0;
+      }
+      // the G probes split [L, U] into G+1 parts: keep the part holding the (j+1)-th eigenvalue
+      double nL = L, nU = U;
+      for (int g2 = 0; g2 < G; ++g2) {
+        const int c2 = __shfl_sync(0xffffffffu, cnt, (lane & ~(G - 1)) + g2, 32);
+        const double x2 = L + (U - L) * (double)(g2 + 1) / (double)(G + 1);
+        if (c2 <= j) nL = x2;
+        else if (x2 < nU) nU = x2;
+      }
+      L = nL;
+      U = nU;
+    }
+    if (act && q == 0) theta[m - 1 - j] = 0.5 * (L + U);     // descending
+  }
+}
+
+inline size_t values_smem_bytes(int m) { return (size_t)(m <= 64 ? 3 : 1) * m * m * sizeof(double); }
 
 inline size_t smem_bytes(int m) {
   const int mm = (m + 1) & ~1;

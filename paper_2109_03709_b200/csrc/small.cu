@@ -323,6 +323,17 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
     cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
     attr = true;
   }
+  if (!R_dev) {                                   // eigenvalues only: tridiagonalisation + multisection
+    static bool vattr = false;
+    if (!vattr) {
+      cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      vattr = true;
+    }
+    ritz::ritz_values_kernel<<<1, 512, ritz::values_smem_bytes(m), stream>>>(S, Bm, m, scr, scr + (size_t)m * m,
+                                                                              theta_dev, c->d_err);
+    PPCA_LAUNCH_CHECK(c, "ritz_values_kernel");
+    return PPCA_OK;
+  }
   const size_t smem = ritz::smem_bytes(m);
   if (m <= 64)
     ritz::ritz_kernel<double><<<1, 512, smem, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, R_dev, c->d_err);
