@@ -515,7 +515,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
     PPCA_TRY(yty(c, Yc, m, n, S));
   }
   // kernel B
-  const int nc = mp <= 64 ? 2 : 1;
+  const int nc = kb::Cfg<64>::NC;
   KBParams bp;
   bp.X = X->data; bp.n = n; bp.d = d; bp.ld = X->ld; bp.m = m; bp.mp = mp;
   bp.ndg = ceil_div(d, nc * 128);
@@ -523,7 +523,15 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   // one work item (d-group × row group) per CTA: the Zᵀ partial stays in TMEM over ~n/(ctas/ndg) rows, so
   // the partials kernel B writes (and reduce_zp reads) are ≈ (ctas/ndg)·d·mp floats
   // (with more d-groups than CTAs, ≥ 4 items per CTA keep the tail short)
-  int64_t want = bp.ndg <= ctas ? std::max<int64_t>(1, ctas / bp.ndg) : ceil_div(4 * ctas, bp.ndg);
+  int64_t want = std::max<int64_t>(1, ctas / bp.ndg);
+  if (bp.ndg > ctas) {                 // ≥ 4 items per CTA; pick the row-group count with the least tail
+    double best = 1e30;
+    for (int64_t r = ceil_div(4 * ctas, bp.ndg); r <= ceil_div(4 * ctas, bp.ndg) + 4; ++r) {
+      const double items = (double)(bp.ndg * r);
+      const double loss = (double)ceil_div(bp.ndg * r, ctas) / (items / (double)ctas);
+      if (loss < best - 1e-9) { best = loss; want = r; }
+    }
+  }
   int64_t rpg = ceil_div(ceil_div(n, want), kb::KR) * kb::KR;
   rpg = std::max<int64_t>(rpg, kb::KR);
   bp.rows_per_rg = rpg;

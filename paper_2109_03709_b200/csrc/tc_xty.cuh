@@ -19,14 +19,18 @@ constexpr uint32_t BLK = KR * 128;            // one 64-column block of a stage 
 // XLO: the X_lo plane of a split X is staged too and X_loᵀ·Y_hi is added (the minibatch steps, whose
 // products are the update itself; the power pass reads X_hi only)
 template <int MP, bool XLO = false> struct Cfg {
-  static constexpr int NC = MP <= 64 ? 2 : 1;             // 128-wide d chunks per work item
+  // 256-column d-groups for every m: the Yᵀ operand (2·MP rows per 64-row stage) is then streamed from L2 once
+  // per 256 X columns (C5, MP = 128: with 128-column groups Yᵀ moved twice X's bytes through L2)
+  static constexpr int NC = 2;                            // 128-wide d chunks per work item
   static constexpr int NB = 2 * MP;                      // UMMA N: [Y_hi; Y_lo]
   static constexpr uint32_t XST = NC * 2 * BLK;          // X stage bytes (one plane)
   static constexpr uint32_t XSTG = XLO ? 2 * XST : XST;  // X stage bytes (all planes)
   static constexpr uint32_t YST = NB * 128;              // Yᵀ stage bytes (NB rows × 64 K)
   static constexpr uint32_t ACC = NC * NB;               // TMEM columns per accumulator buffer
-  static constexpr uint32_t TCOLS = 2 * ACC <= 64 ? 64 : (2 * ACC <= 128 ? 128 : (2 * ACC <= 256 ? 256 : 512));
-  static constexpr int NSTG = XLO ? (int)((227 * 1024 - 1280) / (XSTG + YST)) : NST;
+  static constexpr int NBUF = 2 * ACC <= 512 ? 2 : 1;     // double-buffered items when they fit in TMEM
+  static constexpr uint32_t TCOLS = NBUF * ACC <= 64 ? 64 : (NBUF * ACC <= 128 ? 128 : (NBUF * ACC <= 256 ? 256 : 512));
+  static constexpr int NSTFIT = (int)((227 * 1024 - 1280) / (XSTG + YST));
+  static constexpr int NSTG = NSTFIT < NST ? NSTFIT : NST;
   static constexpr size_t SMEM = 1024 + NSTG * (XSTG + YST) + 256;
 };
 }  // namespace kb
@@ -47,7 +51,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
                   const __grid_constant__ CUtensorMap tmXlo, KBParams p) {
   using namespace kb;
   using CF = Cfg<MP, XLO>;
-  constexpr int NC = CF::NC, NB = CF::NB, NST = CF::NSTG;
+  constexpr int NC = CF::NC, NB = CF::NB, NST = CF::NSTG, NBUF = CF::NBUF;
   constexpr uint32_t XST = CF::XSTG, XPL = CF::XST, YST = CF::YST, ACC = CF::ACC, TCOLS = CF::TCOLS;
   static_assert(!XLO || XBF16, "the X_lo plane is staged by TMA");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
     for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++tt) {
       int64_t r0, nks;
       item_rows(item, r0, nks);
-      const uint32_t b = tt & 1, tph = (tt >> 1) & 1;
+      const uint32_t b = NBUF == 2 ? (tt & 1) : 0, tph = NBUF == 2 ? ((tt >> 1) & 1) : (tt & 1);
       mbar_wait(&tempty[b], tph ^ 1);
       tc_fence_after();
       for (int64_t ks = 0; ks < nks; ++ks, ++it) {
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
       int64_t r0, nks;
       item_rows(item, r0, nks);
       const int64_t dg = item % p.ndg, rg = item / p.ndg;
-      const uint32_t b = tt & 1, tph = (tt >> 1) & 1;
+      const uint32_t b = NBUF == 2 ? (tt & 1) : 0, tph = NBUF == 2 ? ((tt >> 1) & 1) : (tt & 1);
       mbar_wait(&tfull[b], tph);
       tc_fence_after();
       for (int c = 0; c < NC; ++c) {

@@ -42,7 +42,9 @@ struct Cfg {
       TUSED <= 32 ? 32 : (TUSED <= 64 ? 64 : (TUSED <= 128 ? 128 : (TUSED <= 256 ? 256 : 512)));
   static constexpr int PLANES = XM == 2 ? 2 : 1;
   static constexpr uint32_t XSTG = PLANES * XST;
-  static constexpr int NWS = MP <= 64 ? 4 : 2;
+  // W' stages: a 2·MP-row W' chunk is as large as (MP = 64) or twice (MP = 128) the X chunk it multiplies and
+  // comes from L2, so its ring must cover L2 latency too (measured on C5: 2 stages starve the MMA)
+  static constexpr int NWS = MP <= 64 ? 4 : (XM == 1 ? 3 : 2);
   static constexpr uint32_t WST = NB * 128;
   // fp32 Y rows for the CUDA-core S (the tensor-core S keeps the segment sums in registers)
   static constexpr size_t YS = SMMA ? 0 : (size_t)BM * (MP + 4) * 4;
