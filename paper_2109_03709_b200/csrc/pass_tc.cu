@@ -472,6 +472,9 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   static int dbg = -1;
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   fp.dbg = dbg;
+  static int hip = -1;
+  if (hip < 0) hip = getenv("PPCA_FUSED_HI") ? atoi(getenv("PPCA_FUSED_HI")) : 0;
+  fp.hi_policy = hip;
   kernel_timer_mark(c, 0);
   static int cfg = -1;
   if (cfg < 0) cfg = getenv("PPCA_FUSED_CFG") ? atoi(getenv("PPCA_FUSED_CFG")) : 0;

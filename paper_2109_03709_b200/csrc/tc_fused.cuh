@@ -48,6 +48,7 @@ struct KFParams {
   int epoch;
   int pf;                        // A-stream L2 prefetch distance in chunks (0 = off)
   int dbg;                       // experiment switches (PPCA_DBG; 0 in production): 1 skip B-stream
+  int hi_policy;                 // L2 policy of the A-stream's hi plane: 0 evict_last, 1 normal, 2 evict_first
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -160,10 +161,11 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
           if (p.pf) prefetch();
           mbar_wait(&aempty[s], ph ^ 1);
           mbar_arrive_expect_tx(&afull[s], XSTG);
-          if (p.dbg & 2)
+          if (p.hi_policy == 1)
             tma_load_2d(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM));
           else
-            tma_load_2d_hint(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM), keep);
+            tma_load_2d_hint(sA + s * XSTG, &tmX, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM),
+                             p.hi_policy == 2 ? drop : keep);
           if (LO) tma_load_2d_hint(sA + s * XSTG + XPL, &tmXlo, &afull[s], (int32_t)(kc * BK), (int32_t)(t * BM), drop);
         }
       }
