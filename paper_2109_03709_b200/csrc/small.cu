@@ -86,10 +86,17 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
         }
         if (i < ke) A[i * m + j] = lij;
         __syncwarp();
-        // trailing part of the diagonal block: lane ↔ row ii = j+1+lane, columns (j, ii]; l_kk by shuffle
-        for (int kk = j + 1; kk < ke; ++kk) {
-          const double lk = __shfl_sync(0xffffffffu, lij, kk - j - 1);
-          if (i < ke && kk <= i) A[i * m + kk] -= lij * lk;
+        // trailing part of the diagonal block, all lanes at once: lane ↔ (row j+1+(lane&15), columns
+        // j+1+(lane>>4)+2t), t < 8; l_kk by shuffle (independent updates, no serial chain)
+        {
+          const int ir = lane & 15, ii = j + 1 + ir;
+          const double li = __shfl_sync(0xffffffffu, lij, ir);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int co = (lane >> 4) + 2 * t, kk = j + 1 + co;
+            const double lk = __shfl_sync(0xffffffffu, lij, co & 31);
+            if (ii < ke && kk <= ii) A[ii * m + kk] -= li * lk;
+          }
         }
         __syncwarp();
       }
