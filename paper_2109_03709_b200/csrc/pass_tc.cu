@@ -564,9 +564,10 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
 
 void pass_tc_release(Ctx*) {}
 
+ppca_status ritz_debug_clocks(unsigned long long* out8);
 ppca_status debug_wait_counters(unsigned long long* out16) {
-  for (int i = 0; i < 16; ++i) out16[i] = 0;   // wait profiling is compiled out (see tc_xw.cuh history)
-  return PPCA_OK;
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  return ritz_debug_clocks(out16);             // [0..7]: phase timestamps of the last Ritz-values kernel
 }
 
 }  // namespace ppca

@@ -9,6 +9,8 @@
 
 namespace ritz {
 
+__device__ unsigned long long g_ritz_clk[8];   // phase timestamps of the last ritz_values_kernel (profiling)
+
 __device__ __forceinline__ void pair_of(int r, int i, int mm, int& p, int& q) {
   int a, b;
   if (i == 0) {
@@ -176,24 +178,35 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
 // iteration): C = L⁻¹SL⁻ᵀ as above, Householder tridiagonalisation of C (4 barriers per column), then all m
 // eigenvalues of the tridiagonal by Sturm-count multisection (nt/m threads per eigenvalue, 5 sub-intervals
 // per round).  O(m³/nt + m²) instead of Jacobi's O(sweeps·m) barrier rounds.
+//
+// With R != nullptr (m ≤ 64: the refine) the eigenvectors follow too: inverse iteration on the tridiagonal
+// (Gaussian elimination with partial pivoting, 3 steps, clusters of eigenvalues closer than 1e-3·‖T‖ handled
+// by one thread with Gram–Schmidt against the cluster's earlier vectors at every step), back-transformation
+// by the stored Householder reflectors (one thread per vector), then R = Uᵀ L⁻¹ in descending order.
 __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
                                                           int m, double* __restrict__ gLinv, double* __restrict__ gT1,
-                                                          double* __restrict__ theta, int* d_err) {
+                                                          double* __restrict__ theta, int* d_err,
+                                                          double* __restrict__ R = nullptr) {
   extern __shared__ double sm[];
   const bool small = m <= 64;
+  const bool vectors = R != nullptr && small;
   double* A = sm;                                     // m × m (C, then the reduced matrix)
   double* Linv = small ? A + m * m : gLinv;
   double* T1 = small ? A + 2 * m * m : gT1;
   __shared__ double diag0[PPCA_MAX_M], vec[PPCA_MAX_M], pv[PPCA_MAX_M], ta[PPCA_MAX_M], tb[PPCA_MAX_M];
+  __shared__ double hbeta[PPCA_MAX_M], evals[PPCA_MAX_M];
   __shared__ int keep[PPCA_MAX_M];
   __shared__ double sh_alpha, sh_beta, sh_k;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
 
   // 1. L = chol(B), L⁻¹, C = L⁻¹ S L⁻ᵀ (symmetrised)
+  if (tid == 0) g_ritz_clk[0] = clock64();
   for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
   __syncthreads();
   ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err);
+  if (tid == 0) g_ritz_clk[1] = clock64();
   ppca::block_lower_inverse(A, m, keep, Linv);
+  if (tid == 0) g_ritz_clk[2] = clock64();
   for (int e = tid; e < m * m; e += nt) {
     const int j = e / m, i = e % m;
     double s = 0.0;
@@ -217,6 +230,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
     }
   }
   __syncthreads();
+  if (tid == 0) g_ritz_clk[3] = clock64();
   // 2. Householder tridiagonalisation (full symmetric matrix kept up to date)
   for (int k = 0; k + 2 < m; ++k) {
     const int n1 = m - k - 1;
@@ -240,6 +254,10 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
     const double beta = sh_beta;
     for (int i = tid; i < n1; i += nt) vec[i] = i == 0 ? col[0] - sh_alpha : col[i * m];
     __syncthreads();
+    if (vectors) {                                     // reflector k kept in column k below the diagonal
+      for (int i = tid; i < n1; i += nt) A[(k + 1 + i) * m + k] = vec[i];
+      if (tid == 0) hbeta[k] = beta;
+    }
     if (beta != 0.0) {
       // p = β C' v, C' = A[k+1.., k+1..]: G threads per row (consecutive lanes), shuffle-reduced
       // (uniform trip counts per warp: every lane reaches the shuffles)
@@ -285,6 +303,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
     ta[m - 1] = A[(m - 1) * m + (m - 1)];
   }
   __syncthreads();
+  if (tid == 0) g_ritz_clk[4] = clock64();
   // 3. Sturm multisection: eigenvalue j (ascending) by G = nt/m threads; count(x) = #{i : d_i < 0}
   double lo = 0.0, hi = 0.0;
   for (int i = 0; i < m; ++i) {                        // Gershgorin bounds (every thread)
@@ -306,9 +325,9 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
       const double x = L + (U - L) * (double)(q + 1) / (double)(G + 1);
       int cnt = 0;
       double dd = 1.0;
-      for (int i = 0; i < (act ? m : 0); ++i) {
+      for (int i = 0; i < (act ? m : 0); ++i) {      // (reciprocal instead of an IEEE division: only signs count)
         const double bs = i > 0 ? tb[i - 1] * tb[i - 1] : 0.0;
-        dd = (ta[i] - x) - (i > 0 ? bs / dd : 0.0);
+        dd = (ta[i] - x) - (i > 0 ? bs * __drcp_rn(dd) : 0.0);
         if (dd == 0.0) dd = -1e-300;
         cnt += dd < 0.0;
       }
@@ -323,7 +342,104 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
       L = nL;
       U = nU;
     }
-    if (act && q == 0) theta[m - 1 - j] = 0.5 * (L + U);     // descending
+    if (act && q == 0) {
+      theta[m - 1 - j] = 0.5 * (L + U);                // descending
+      evals[j] = 0.5 * (L + U);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_ritz_clk[5] = clock64();
+  if (!vectors) return;
+  // 4. eigenvectors of T: inverse iteration, one thread per cluster of close eigenvalues
+  double* XT = T1;                                    // XT[i·m + j] = component i of eigenvector j (ascending)
+  const double ctol = 1e-3 * fmax(fabs(lo), fabs(hi));
+  const double tiny = 1e-14 * span;
+  for (int j0 = tid; j0 < m; j0 += nt) {
+    if (j0 > 0 && evals[j0] - evals[j0 - 1] <= ctol) continue;   // not a cluster leader
+    int j1 = j0 + 1;
+    while (j1 < m && evals[j1] - evals[j1 - 1] <= ctol) ++j1;
+    for (int j = j0; j < j1; ++j) {
+      double dl[PPCA_MAX_M / 2], d[PPCA_MAX_M / 2], du[PPCA_MAX_M / 2], du2[PPCA_MAX_M / 2], x[PPCA_MAX_M / 2];
+      bool sw[PPCA_MAX_M / 2];
+      const double sg = evals[j];
+      for (int i = 0; i < m; ++i) {
+        d[i] = ta[i] - sg;
+        if (i + 1 < m) { du[i] = tb[i]; dl[i] = tb[i]; }
+        du2[i] = 0.0;
+        sw[i] = false;
+      }
+      for (int i = 0; i + 1 < m; ++i) {              // tridiagonal LU with partial pivoting
+        if (fabs(d[i]) >= fabs(dl[i])) {
+          if (d[i] == 0.0) d[i] = tiny;
+          const double f = dl[i] / d[i];
+          dl[i] = f;
+          d[i + 1] -= f * du[i];
+        } else {
+          const double f = d[i] / dl[i];
+          d[i] = dl[i];
+          dl[i] = f;
+          const double t = du[i];
+          du[i] = d[i + 1];
+          d[i + 1] = t - f * d[i + 1];
+          if (i + 2 < m) {
+            du2[i] = du[i + 1];
+            du[i + 1] = -f * du[i + 1];
+          }
+          sw[i] = true;
+        }
+      }
+      if (fabs(d[m - 1]) < tiny) d[m - 1] = d[m - 1] < 0.0 ? -tiny : tiny;
+      for (int i = 0; i < m; ++i) x[i] = 1.0 + 0.37 * sin(0.9 * (double)(i + 1) * (double)(j + 1));
+      for (int it = 0; it < 3; ++it) {
+        for (int i = 0; i + 1 < m; ++i) {              // L
+          if (!sw[i]) {
+            x[i + 1] -= dl[i] * x[i];
+          } else {
+            const double t = x[i];
+            x[i] = x[i + 1];
+            x[i + 1] = t - dl[i] * x[i];
+          }
+        }
+        x[m - 1] /= d[m - 1];                          // U
+        if (m >= 2) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) / (fabs(d[m - 2]) < tiny ? tiny : d[m - 2]);
+        for (int i = m - 3; i >= 0; --i)
+          x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / (fabs(d[i]) < tiny ? tiny : d[i]);
+        for (int jp = j0; jp < j; ++jp) {              // Gram–Schmidt against the cluster's earlier vectors
+          double dt = 0.0;
+          for (int i = 0; i < m; ++i) dt += XT[i * m + jp] * x[i];
+          for (int i = 0; i < m; ++i) x[i] -= dt * XT[i * m + jp];
+        }
+        double nn = 0.0;
+        for (int i = 0; i < m; ++i) nn += x[i] * x[i];
+        const double rn = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        for (int i = 0; i < m; ++i) x[i] *= rn;
+      }
+      for (int i = 0; i < m; ++i) XT[i * m + j] = x[i];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_ritz_clk[6] = clock64();
+  // 5. back-transformation y = H_0 ⋯ H_{m-3} x (one thread per vector; reflector reads are broadcasts)
+  for (int j = tid; j < m; j += nt) {
+    for (int k = m - 3; k >= 0; --k) {
+      const double bk = hbeta[k];
+      if (bk == 0.0) continue;
+      const int n1 = m - k - 1;
+      double dt = 0.0;
+      for (int i = 0; i < n1; ++i) dt += A[(k + 1 + i) * m + k] * XT[(k + 1 + i) * m + j];
+      dt *= bk;
+      for (int i = 0; i < n1; ++i) XT[(k + 1 + i) * m + j] -= dt * A[(k + 1 + i) * m + k];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_ritz_clk[7] = clock64();
+  // 6. R = Uᵀ L⁻¹ in descending order (row i ↔ ascending eigenvector m-1-i)
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, c = e % m;
+    const int j = m - 1 - i;
+    double sum = 0.0;
+    for (int t = c; t < m; ++t) sum += XT[t * m + j] * Linv[t * m + c];
+    R[e] = sum;
   }
 }
 

@@ -320,6 +320,12 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
 // ============================================================================ Rayleigh–Ritz (one CTA)
 #include "ritz.cuh"
 
+ppca_status ritz_debug_clocks(unsigned long long* out8) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, ritz::g_ritz_clk, 8 * sizeof(unsigned long long));
+  return PPCA_OK;
+}
+
 ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev, double* R_dev,
                        cudaStream_t stream) {
   double* scr = (double*)scratch(c, S_EVAL, (size_t)2 * m * m * sizeof(double));
@@ -330,14 +336,16 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
     cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
     attr = true;
   }
-  if (!R_dev) {                                   // eigenvalues only: tridiagonalisation + multisection
+  static int jacobi = -1;                         // PPCA_RITZ_JACOBI=1: the Jacobi solver for vectors too
+  if (jacobi < 0) jacobi = getenv("PPCA_RITZ_JACOBI") ? atoi(getenv("PPCA_RITZ_JACOBI")) : 0;
+  if (!R_dev || (m <= 64 && !jacobi)) {           // tridiagonalisation + multisection (+ inverse iteration)
     static bool vattr = false;
     if (!vattr) {
       cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       vattr = true;
     }
     ritz::ritz_values_kernel<<<1, 512, ritz::values_smem_bytes(m), stream>>>(S, Bm, m, scr, scr + (size_t)m * m,
-                                                                              theta_dev, c->d_err);
+                                                                              theta_dev, c->d_err, R_dev);
     PPCA_LAUNCH_CHECK(c, "ritz_values_kernel");
     return PPCA_OK;
   }
