@@ -409,6 +409,7 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
     } else {
       float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, rows) * m * sizeof(float));
       if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+      c->last_impl = 1;
       PPCA_TRY(xw(c, X, r0, rows, W, m, Y));
       PPCA_TRY(ytx(c, X, r0, rows, Y, m, Q));
       PPCA_TRY(yty(c, Y, m, rows, P));

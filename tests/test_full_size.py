@@ -1,5 +1,6 @@
-"""Full-size checks (BASELINE.json configs[2] = C3 and configs[4] = C5) in the launch configuration bench.py
-times: the split / bf16 X on one GPU, the tcgen05 pass, power priming with per-iterate Ritz values, refine.
+"""Full-size checks of BASELINE.json configs[1..4] (C2, C3, C4, C5) in the launch configuration bench.py
+times: the split / bf16 X on one GPU, the tcgen05 pass, power priming with per-iterate Ritz values,
+minibatch primings, refine.  C2 (60000 x 784) is small enough for the fp64 oracle itself.
 
 The fp64 oracle cannot stream these sizes in seconds, so the checks are (i) outputs it can compute one by
 one — generator rows sampled across the shard, including the ragged last tile — and (ii) properties that
@@ -166,3 +167,82 @@ def test_c5_full_size(P, ctx):
         assert U.ritz_rel_err(h2[t], h1[t]) < tol, f"iteration {t}"
     assert U.ritz_rel_err(th2, th1) < tol
     _properties(P, ctx, Xm, w, W2, h2, E2, th2, tol)
+
+
+def test_c2_full_size_oja_against_oracle(P, ctx):
+    """C2 (BASELINE configs[1]) at its full size, 60000 x 784, against the fp64 oracle directly: the whole
+    stored X, 10 epochs (2350 steps) of generalized Oja (b = 256, α = 1e-3, Nesterov 0.9; readings R8-R10),
+    the pPCA refine (Ritz values 1e-4, |cos| where gapped, identical LCES)."""
+    import torch
+    from oracle import ppca_oracle as O
+    w = C.C2
+    s = w.spec
+    Xs = G.dataset(s)
+    X64 = G.stored_to_f64(Xs, s.dtype)
+    lam, T = O.truth(X64)
+    steps = 2350
+    W_ref, _ = O.prime_oja(X64, G.init_gaussians(w.init_seed, w.m, s.d), w.batch, w.alpha, w.momentum, steps)
+    E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, W_ref, w.k)
+    X = torch.empty((s.n, s.d), dtype=torch.float32, device="cuda")
+    P.ppca_generate(ctx, P.gen_spec(s), X)
+    np.testing.assert_array_less(np.abs(X.cpu().numpy() - Xs), np.spacing(np.abs(Xs)) * 1.01 + 1e-30)
+    P.ppca_split_f32(ctx, X, s.d)
+    Xm = P.matrix(X, split=True)
+    W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+    vel = torch.zeros_like(W)
+    assert P.ppca_prime_oja(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, w.init_seed, W, vel, 0) == steps
+    rel = np.linalg.norm(W.cpu().numpy() - W_ref) / np.linalg.norm(W_ref)
+    assert rel < 1e-3, f"Oja trajectory drift {rel:.2e}"
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    th, _ = P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
+    err = U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, 1e-4, "C2 full", th_all_ref)
+    lc, _ = U.lces_all(E.cpu().numpy(), T[: w.k])
+    print(f"\n[parity] C2 full: Oja drift {rel:.2e}, Ritz rel err {err:.3e}, LCES {lc}")
+
+
+def test_c4_full_size_eigengame_properties(P, ctx):
+    """C4 (BASELINE configs[3]) at its full size, 2·10⁶ x 4096 fp32 (split layout, 32.8 GB): EigenGame steps
+    on the tensor-core window pass against the exact-fp32 CUDA-core pass from the same start, then the
+    refine's properties (idempotence, captured variance = θ, Ky Fan) and Cauchy interlacing with the exact
+    spectrum of XᵀX (fp64 Gram over all rows)."""
+    import torch
+    w = C.C4
+    s = w.spec
+    X = torch.empty((s.n, s.d), dtype=torch.float32, device="cuda")
+    _, mu = P.ppca_generate(ctx, P.gen_spec(s), X)
+    _check_rows(X, mu, s)
+    G64 = torch.zeros((s.d, s.d), dtype=torch.float64, device="cuda")
+    P.ppca_gram(ctx, P.matrix(X), G64)
+    lam = np.linalg.eigvalsh(G64.cpu().numpy())[::-1]
+    del G64
+    P.ppca_split_f32(ctx, X, s.d)
+    Xm = P.matrix(X, split=True)
+    steps = 20
+    out = {}
+    for impl in (1, 2):
+        P.ppca_set_pass_impl(ctx, impl)
+        try:
+            V = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+            vel = torch.zeros_like(V)
+            P.ppca_prime_eigengame(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, w.init_seed, V, vel, 0)
+            out[impl] = (V.clone(), P.ppca_last_pass_impl(ctx))
+        finally:
+            P.ppca_set_pass_impl(ctx, 0)
+    assert out[1][1] == 1 and out[2][1] == 2
+    V1, V2 = out[1][0].cpu().numpy().astype(np.float64), out[2][0].cpu().numpy().astype(np.float64)
+    rel = np.linalg.norm(V2 - V1) / np.linalg.norm(V1)
+    assert rel < 1e-3, f"tensor-core vs CUDA-core EigenGame trajectories differ by {rel:.2e}"
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    V = out[2][0]
+    th, dim = P.ppca_refine(ctx, Xm, V, w.m, w.k, E)
+    assert dim == w.m
+    tol = 1e-4
+    d, m = s.d, w.m
+    for i in range(w.k):
+        assert lam[i + d - m] * (1 - tol) <= th[i] <= lam[i] * (1 + tol)
+    E2 = torch.zeros_like(E)
+    th2, _ = P.ppca_refine(ctx, Xm, E, w.k, w.k, E2)
+    assert U.ritz_rel_err(th2, th) < tol
+    var = P.ppca_captured_variance(ctx, Xm, E, w.k)
+    np.testing.assert_allclose(var, th, rtol=tol)
+    print(f"\n[parity] C4 full: EigenGame TC vs SIMT drift {rel:.2e}, theta_1/lambda_1 {th[0] / lam[0]:.6f}")
