@@ -30,7 +30,7 @@ if ROOT not in sys.path:
 METRIC = "X-pass HBM GB/s (% of peak) and pPCA time-to-LCES at 1/2/4/8 B200"
 LCES_TARGET = {"C1": math.pi / 1024, "C3": math.pi / 1024, "C5": math.pi / 8}   # reading R20
 CFG_INDEX = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}
-DESCR = {"C1": "tiny planted exp spectrum", "C3": "planted exp spectrum λ_j=e^(-j/20)",
+DESCR = {"C1": "tiny planted exp spectrum", "C2": "image-like sparse factor model", "C4": "power-law spectrum", "C3": "planted exp spectrum λ_j=e^(-j/20)",
          "C5": "wide activation-like (Householder r=8, ReLU, λ_j=1/j)"}
 
 
@@ -343,6 +343,163 @@ def run_ours(args, w, rank, world, local_rank):
     return 0
 
 
+# ----------------------------------------------------------------------------- minibatch primings (C2, C4)
+def oracle_minibatch_rate(w, rows: int, steps: int):
+    """The fp64 oracle's minibatch step (Oja / EigenGame) on the first `rows` rows; GB/s of stored X."""
+    from inputs import generate as G
+    from oracle import ppca_oracle as O
+    X = _oracle_sample(w, rows)
+    V = O.init_vectors(G.init_gaussians(w.init_seed, w.m, w.spec.d))
+    vel = np.zeros_like(V)
+    step = O.oja_step if w.priming == "oja" else O.eigengame_step
+    b = min(w.batch, rows)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        r0 = (k * b) % max(1, rows - b + 1)
+        V, vel = step(X[r0:r0 + b], V, vel, w.alpha, w.momentum)
+    dt = (time.perf_counter() - t0) / steps
+    return b * w.spec.d * 4 / dt / 1e9, dt
+
+
+def run_minibatch(args, w, rank, world, local_rank):
+    """One step = one minibatch priming step (P L70-72 generalized Oja, or P L76-88 EigenGame) over the
+    global batch: the window pass (Y = X_b·W'ᵀ, Q = X_bᵀY, P = YᵀY), the all-reduce (N>1) and the update.
+    value = X bytes of the global batch per step ÷ step time (the batch is re-read every step)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2109_03709_b200 as P
+    P.load()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+    ctx = P.ppca_ctx_create_distributed(local_rank, stream)
+    P.ppca_set_pass_impl(ctx, {"auto": 0, "simt": 1, "tc": 2}[args.pass_impl])
+    s = w.spec
+    split = s.dtype == "f32" and args.storage == "split"
+    layout = P.PPCA_LAYOUT_INTERLEAVED if world > 1 else P.PPCA_LAYOUT_CONTIGUOUS
+    from inputs import generate as G
+    n_local = len(G.shard_rows(s.n, rank, world, "interleaved" if world > 1 else "contiguous", w.batch))
+    X = torch.empty((max(n_local, 1), s.d), dtype=torch.float32, device=dev)[:n_local]
+    P.ppca_generate(ctx, P.gen_spec(s, layout=layout, block_rows=w.batch if world > 1 else 0, split=split), X)
+    Xm = P.matrix(X, n_global=s.n, d=s.d, split=split, layout=layout, block_rows=w.batch if world > 1 else 0)
+    fn = P.ppca_prime_oja if w.priming == "oja" else P.ppca_prime_eigengame
+    V = torch.empty((w.m, s.d), dtype=torch.float32, device=dev)
+    vel = torch.zeros_like(V)
+    steps = max(args.steps, 1) * (20 if w.priming == "oja" else 5)     # ≥ 50 steps (µs-scale steps)
+    step0 = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, max(args.warmup, 3), w.init_seed, V, vel, 0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    P.ppca_set_timing(ctx, True)
+    P.ppca_get_pass_time(ctx), P.ppca_get_kernel_time(ctx, 0), P.ppca_get_kernel_time(ctx, 1)
+    l0 = P.ppca_launch_count(ctx)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, 0, V, vel, step0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = P.ppca_launch_count(ctx) - l0
+    pass_ms_tot, passes = P.ppca_get_pass_time(ctx)
+    ka_ms, ka_n = P.ppca_get_kernel_time(ctx, 0)
+    kb_ms, kb_n = P.ppca_get_kernel_time(ctx, 1)
+    P.ppca_set_timing(ctx, False)
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms / steps
+    batch_bytes = w.batch * s.d * 4
+    value = batch_bytes / (ms_step / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    local_batch = w.batch // world
+    if ka_n or kb_n:       # the tensor-core window pass: kernel A2 (K-split) and the precise kernel B
+        cand = [("xw_tma_kernel (kernel A2, K-split over the step's window)", ka_ms, ka_n),
+                ("xty_tc_kernel (kernel B, X_hi and X_lo planes)", kb_ms, kb_n)]
+        kname, k_tot, k_n = max(cand, key=lambda k: k[1])
+        k_ms = max_over_ranks(k_tot / max(k_n, 1))
+        k_bytes = local_batch * s.d * 4
+    elif launches == 1:    # short windows on one GPU: every step inside one cooperative kernel
+        kname, k_ms, k_n, k_bytes = "oja_persistent_kernel (all steps in one cooperative launch; grid-barrier " \
+            "latency bound)", ms_step, steps, local_batch * s.d * 4
+    else:                  # small windows run the CUDA-core kernels: the whole (launch-bound) step is reported
+        kname, k_ms, k_n, k_bytes = "minibatch step (CUDA-core window kernels; launch-latency bound)", ms_step, \
+            steps, local_batch * s.d * 4
+    achieved = k_bytes / (k_ms / 1e3) / 1e9
+    ttl = None
+    if not args.no_lces and world == 1 and s.d <= 4096:
+        G64 = torch.zeros((s.d, s.d), dtype=torch.float64, device=dev)
+        P.ppca_gram(ctx, P.matrix(X, split=split), G64)
+        lam, U = np.linalg.eigh(G64.cpu().numpy())
+        del G64
+        Tt = torch.from_numpy(U[:, ::-1][:, : w.k].T.copy().astype(np.float32)).to(dev)
+        thr = math.pi / 8                               # reading R20 for the minibatch configs
+        V2 = torch.empty_like(V)
+        vel2 = torch.zeros_like(V)
+        E = torch.empty((w.k, s.d), dtype=torch.float32, device=dev)
+        per_epoch = -(-s.n // w.batch)
+        checkpoints = sorted(set([2 ** j for j in range(4, 13)] + [per_epoch * e for e in range(1, 31)]))
+        cap = 30 * per_epoch if w.priming == "oja" else 4096       # reading R21
+        step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, 0, w.init_seed, V2, vel2, 0)
+        reached, t_ms = None, 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for cp in checkpoints:
+            if cp > cap:
+                break
+            e0.record(stream)
+            step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, cp - step, 0, V2, vel2, step)
+            P.ppca_refine(ctx, Xm, V2, w.m, w.k, E)                  # charged refine (S L429)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_ms += e0.elapsed_time(e1)
+            _, lc = P.ppca_eval(ctx, E, Tt, w.k, s.d, [thr])
+            if lc[0] >= w.k:
+                reached = cp
+                break
+        ttl = {"target": f"LCES={w.k} at V={thr:.6f}", "steps": reached,
+               "ms": t_ms if reached else None, "checkpoints": "2^j and every epoch, refine charged"}
+    P.ppca_ctx_destroy(ctx)
+    if rank != 0:
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rows = min(s.n, w.batch * (16 if w.priming == "oja" else 1))    # host generation of the sample is costly
+        ksteps = 200 if w.priming == "oja" else 10
+        gbs, dt_s = oracle_minibatch_rate(w, rows, ksteps)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{ksteps} fp64 numpy oracle {w.priming} steps (batch {min(w.batch, rows)}) on {rows} of "
+                         f"{s.n} rows of {w.name} ({dt_s * 1e3:.1f} ms/step)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": s.dtype, "data": "synthetic",
+        "config": {"workload": f"{w.name} (BASELINE.json configs[{CFG_INDEX.get(w.name, '?')}]): {w.priming} priming, "
+                               f"n={s.n}, d={s.d}, batch={w.batch}, alpha={w.alpha}, momentum={w.momentum}, "
+                               f"k={w.k}, l={w.l}",
+                   "n": s.n, "d": s.d, "m": w.m, "k": w.k, "priming": w.priming, "batch": w.batch,
+                   "storage": "f32 split (bf16 hi/lo planes, 4 B/elt)" if split else s.dtype,
+                   "parallelism": f"dp{world} (interleaved block rows, NCCL all-reduce of Q,P per step)",
+                   "l2": f"batch {batch_bytes / 1e6:.1f} MB per step re-read from HBM/L2 (X {s.n * s.d * 4 / 1e9:.2f} GB)",
+                   "step": "window pass + all-reduce + update (one minibatch step)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": kname, "kernel_ms": k_ms, "launches": k_n,
+                     "algorithmic_bytes_per_launch": k_bytes, "peak_source": peak_src},
+        "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(),
+        "time_to_lces": ttl,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,19 +518,19 @@ def main():
     args = ap.parse_args()
     from inputs import configs as C
     w = C.FULL[args.config] if args.config in C.FULL else C.SMALL[args.config]
-    if w.priming != "power":
-        raise SystemExit("bench.py times the block-power step; use a power-primed config (C1, C3, C5)")
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
+        if w.priming != "power":
+            raise SystemExit("--impl reference times the power step (C1, C3, C5)")
         return run_reference(args, w, rank)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    rc = run_ours(args, w, rank, world, local_rank)
+    rc = (run_ours if w.priming == "power" else run_minibatch)(args, w, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
-SOURCES = ["api.cu", "gemm_simt.cu", "small.cu", "gen.cu", "pass.cu", "pass_tc.cu"]
+SOURCES = ["api.cu", "gemm_simt.cu", "small.cu", "gen.cu", "pass.cu", "pass_tc.cu", "oja_persistent.cu"]
 
 
 def _newer(src_list, target):

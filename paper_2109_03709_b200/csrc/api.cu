@@ -391,6 +391,16 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
   double* P = (double*)scratch(c, S_S, (size_t)m * m * sizeof(double));
   if (!Q || !P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   int64_t s0 = *step_io;
+  if (!eigengame) {
+    // short windows on one GPU: every step inside one persistent kernel (the multi-launch step below is
+    // launch-latency bound there)
+    ppca_status pst;
+    if (oja_persistent(c, X, m, batch, alpha, mu, s0, steps, W, vel, &pst)) {
+      PPCA_TRY(pst);
+      *step_io = s0 + steps;
+      return PPCA_OK;
+    }
+  }
   const size_t row_bytes = (size_t)X->ld * elt_size(X->dtype);
   for (int64_t s = s0; s < s0 + steps; ++s) {
     int64_t r0, rows;

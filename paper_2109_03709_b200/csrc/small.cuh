@@ -34,6 +34,10 @@ ppca_status normalize_rows(Ctx* c, float* W, int m, int64_t d);
 // Oja / Sanger update (fp64 per element):  G = Q − tril(P)·W;  v ← μv + G;  W ← W + α(G + μv).
 ppca_status oja_update(Ctx* c, const float* Q, const double* P, float* W, float* vel, int m,
                        int64_t d, double alpha, double mu);
+// Generalized Oja, all `steps` steps in one cooperative kernel (oja_persistent.cu): single GPU, m ≤ 64,
+// short windows, automatic pass selection.  Returns false (nothing launched) when not applicable.
+bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha, double mu, int64_t s0,
+                    int64_t steps, float* W, float* vel, ppca_status* st);
 // EigenGame update: coefficients from A, r = 2MV − 2 N·MV − 2U∘V, Nesterov, renormalise.
 ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m,
                              int64_t d, double alpha, double mu);

@@ -188,9 +188,11 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
 
 
 # ----------------------------------------------------------------------------- minibatch primings
-@pytest.mark.parametrize("impl", [0, 2], indirect=True, ids=["auto", "tcgen05"])
+@pytest.mark.parametrize("impl", [0, 1, 2], indirect=True, ids=["auto", "simt", "tcgen05"])
 @pytest.mark.parametrize("split", [False, True], ids=["f32", "split"])
 def test_oja_parity_c2s(P, ctx, split, impl):
+    """C2s (ragged last minibatch: 12096 = 47·256 + 64): auto = the persistent single-kernel Oja
+    (oja_persistent.cu), simt = one launch sequence per step, tcgen05 = the tensor-core window pass."""
     import torch
     w = C.SMALL["C2s"]
     s = w.spec
@@ -211,6 +213,27 @@ def test_oja_parity_c2s(P, ctx, split, impl):
     E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
     th, dim = P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), "C2s", th_all_ref)
+
+
+def test_oja_persistent_resume_bit_exact(P, ctx):
+    """The persistent Oja kernel is deterministic and resumable: 200 steps in one call equal 77 + 123 steps
+    through step_io (same W and velocity bits), and the step counter wraps over the epoch boundary."""
+    import torch
+    w = C.SMALL["C2s"]
+    s = w.spec
+    Xs, _ = _host(w)
+    Xm = _device_matrix(P, ctx, Xs, s, True)
+    outs = []
+    for chunks in ([200], [77, 123]):
+        W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+        vel = torch.zeros_like(W)
+        step = 0
+        for i, c in enumerate(chunks):
+            step = P.ppca_prime_oja(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, c, w.init_seed if i == 0 else 0,
+                                    W, vel, step)
+        assert step == 200
+        outs.append((W.cpu().numpy(), vel.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
 @pytest.mark.parametrize("impl", [0, 2], indirect=True, ids=["auto", "tcgen05"])
