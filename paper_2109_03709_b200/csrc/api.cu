@@ -320,16 +320,18 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   float* Z = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
   double* Sbuf = (double*)scratch(c, S_S, (size_t)4 * m * m * sizeof(double));      // S[2], Bm[2]
   double* theta_dev = (double*)scratch(c, S_TC2, (size_t)std::max(1, iters) * m * sizeof(double) + (size_t)m * m * sizeof(double));
-
   if (!Z || !Sbuf || !theta_dev) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, m, &plan));
   // pre-touch the scratch the loop uses so no allocation happens while the side stream is busy
   if (!scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double)) || !scratch(c, S_GRAM, (size_t)m * m * sizeof(double)) ||
       !scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64) ||
-      !scratch(c, S_W2, (size_t)m * d * sizeof(float)))
+      !scratch(c, S_W2, (size_t)m * d * sizeof(float)) || !scratch(c, S_SIDE_PART, vec_gram_part_bytes(c, m, d)))
     return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  cudaEvent_t ev_main[2], ev_side[2];
+  cudaEvent_t ev_main[2], ev_side[2], ev_prep, ev_gram;
+  cudaEventCreateWithFlags(&ev_prep, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_gram, cudaEventDisableTiming);
+  cudaEventRecord(ev_gram, c->side);
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&ev_main[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_side[i], cudaEventDisableTiming);
@@ -337,33 +339,45 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   }
   ppca_status st = PPCA_OK;
   c->side_busy = theta_hist_host != nullptr;
+  c->prep_ev = theta_hist_host ? ev_prep : nullptr;
   for (int t = 0; t < iters && st == PPCA_OK; ++t) {
     double* S = Sbuf + (size_t)(t & 1) * m * m;
     double* Bm = Sbuf + (size_t)(2 + (t & 1)) * m * m;
-    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);
+    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);   // Ritz t-2 done with S, Bm
     st = pass_power(c, X, &plan, W, m, Z, S);               // Z = YᵀX, S = YᵀY  (local)
     if (st != PPCA_OK) break;
+    if (theta_hist_host) {
+      // side stream: Bm = W'W'ᵀ of the operand the pass uses (from ev_prep on, overlapping the pass), then
+      // the pPCA-for-free Ritz values of span(W'_t) once S_t is reduced
+      cudaStreamWaitEvent(c->side, ev_prep, 0);
+      st = vec_gram_on(c, plan.Wop, m, d, Bm, c->side, S_SIDE_PART);
+      if (st != PPCA_OK) break;
+      cudaEventRecord(ev_gram, c->side);
+    }
     st = allreduce(c, Z, (size_t)m * d, false);
     if (st == PPCA_OK) st = allreduce(c, S, (size_t)m * m, true);
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
-      st = vec_gram(c, plan.Wop, m, d, Bm);
-      if (st != PPCA_OK) break;
       cudaEventRecord(ev_main[t & 1], c->stream);
       cudaStreamWaitEvent(c->side, ev_main[t & 1], 0);
       st = ritz_solve(c, S, Bm, m, theta_dev + (size_t)t * m, nullptr, c->side);   // values only
       cudaEventRecord(ev_side[t & 1], c->side);
       if (st != PPCA_OK) break;
     }
-    // W ← orth(Z): one fp64 Cholesky-QR pass (κ(Z)² ε64 ≪ fp32 rounding for power iterates)
+    // W ← orth(Z): one fp64 Cholesky-QR pass (κ(Z)² ε64 ≪ fp32 rounding for power iterates); it rewrites
+    // W (the SIMT pass's operand) and the next prep_w rewrites W' — after the side-stream Gram has read it
+    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_gram, 0);
     st = cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
   }
+  c->prep_ev = nullptr;
   c->side_busy = false;
   ppca_status st2 = finish(c, "ppca_prime_power");
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(ev_main[i]);
     cudaEventDestroy(ev_side[i]);
   }
+  cudaEventDestroy(ev_prep);
+  cudaEventDestroy(ev_gram);
   if (st != PPCA_OK) return st;
   if (st2 != PPCA_OK) return st2;
   if (theta_hist_host && iters > 0) {

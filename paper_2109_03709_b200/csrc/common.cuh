@@ -30,6 +30,7 @@ struct Ctx {
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // side stream (Ritz solves overlap the next pass)
+  cudaEvent_t prep_ev = nullptr;     // when set: recorded once the pass operand W' is prepared (power loop)
   bool side_busy = false;             // side-stream kernels may overlap the next pass: persistent
                                       // pass kernels then leave one SM free (a late CTA stalls the pass)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -71,6 +72,8 @@ enum Slot {
   S_EVAL,
   S_TC0, S_TC1, S_TC2, S_TC3, S_TC4,   // tensor-core pass scratch
   S_TILES,                         // row-tile list of the subsampled refine (int32)
+  S_SIDE,                          // side-stream m×m work of the power loop (Linv[2], row maps)
+  S_SIDE_PART,                     // side-stream split partials (vector Gram)
   S_NTSTAGE,
 };
 
@@ -177,6 +180,43 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// s = Σ load(i) for i = begin, begin + step, … < end, added in exactly that order (bit-identical to the plain
+// loop) but with U loads in flight before the adds: a plain accumulation loop waits a full L2/HBM round
+// trip per term when the compiler does not hoist the loads.
+template <int U, typename L>
+__device__ __forceinline__ double sum_in_order(int64_t begin, int64_t end, int64_t step, L load) {
+  double s = 0.0;
+  int64_t i = begin;
+  for (; i + (U - 1) * step < end; i += U * step) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = load(i + u * step);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u];
+  }
+  for (; i < end; i += step) s += load(i);
+  return s;
+}
+
+// store(e, load(e)) for e = first, first + stride, … < count with U loads in flight before the stores
+// (out-of-range lanes of the last batch load element count − 1 and store nothing).
+template <int U, typename L, typename S>
+__device__ __forceinline__ void copy_batched(int64_t first, int64_t count, int64_t stride, L load, S store) {
+  for (int64_t e0 = first; e0 < count; e0 += U * stride) {
+    decltype(load(e0)) v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      v[u] = load(e < count ? e : count - 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < count) store(e, v[u]);
+    }
+  }
 }
 
 }  // namespace ppca

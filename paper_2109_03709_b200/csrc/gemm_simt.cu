@@ -275,9 +275,7 @@ __global__ void reduce_splits_f64_kernel(const double* __restrict__ P, int nspli
                                          double* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  double s = 0.0;
-  for (int z = 0; z < nsplit; ++z) s += P[(int64_t)z * count + i];
-  out[i] = s;
+  out[i] = sum_in_order<8>(0, nsplit, 1, [&](int64_t z) { return P[z * count + i]; });
 }
 
 ppca_status launch_reduce_splits_f32(Ctx* c, const double* P, int nsplit, int64_t count, float* out,
@@ -290,8 +288,13 @@ ppca_status launch_reduce_splits_f32(Ctx* c, const double* P, int nsplit, int64_
 }
 
 ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_t count, double* out) {
+  return launch_reduce_splits_f64(c, P, nsplit, count, out, c->stream);
+}
+
+ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_t count, double* out,
+                                     cudaStream_t st) {
   if (count <= 0) return PPCA_OK;
-  reduce_splits_f64_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, c->stream>>>(P, nsplit, count, out);
+  reduce_splits_f64_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(P, nsplit, count, out);
   PPCA_LAUNCH_CHECK(c, "reduce_splits_f64");
   return PPCA_OK;
 }

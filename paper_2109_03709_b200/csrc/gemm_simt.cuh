@@ -25,5 +25,7 @@ int tn_pick_splits(Ctx* c, int64_t M, int64_t N, int64_t K);
 ppca_status launch_reduce_splits_f32(Ctx* c, const double* P, int nsplit, int64_t count, float* out,
                                      int64_t ldo, int64_t cols);
 ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_t count, double* out);
+ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_t count, double* out,
+                                     cudaStream_t st);
 
 }  // namespace ppca

@@ -148,6 +148,7 @@ ppca_status pass_time_collect(Ctx* c, double* ms, int64_t* n) {
 static ppca_status pass_power_impl(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m,
                                    float* Z, double* S) {
   if (plan->impl == 2) return pass_tc_power(c, X, plan, W, m, Z, S, plan->precise);
+  if (c->prep_ev) cudaEventRecord(c->prep_ev, c->stream);     // the operand is W itself
   float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * m * sizeof(float));
   if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   if (X->n_local == 0) {

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) reduce_spart_kernel(const double* __restr
   if (e < m * m) {
     const int i = e / m, j = e % m;
     const int idx = min(i, j) * mp + max(i, j);   // partials hold the upper triangle, dense [mp][mp]
-    for (int c = warp; c < nparts; c += 8) s += Spart[(int64_t)c * mp * mp + idx];
+    s = sum_in_order<8>(warp, nparts, 8, [&](int64_t c) { return Spart[c * mp * mp + idx]; });
   }
   part[warp][lane] = s;
   __syncthreads();
@@ -140,10 +140,10 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
   if (e < m * m) {
     const int i = e / m, j = e % m;
     const int a = min(i, j), b = max(i, j);
-    for (int c = warp; c < nparts; c += 8) {
-      const double* P = Spart + (int64_t)c * 2 * mp * mp;
-      s += P[a * mp + b] + P[(a + mp) * mp + b];
-    }
+    s = sum_in_order<8>(warp, nparts, 8, [&](int64_t c) {
+      const double* P = Spart + c * 2 * mp * mp;
+      return P[a * mp + b] + P[(a + mp) * mp + b];
+    });
   }
   part[warp][lane] = s;
   __syncthreads();
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict_
   const int j = blockIdx.y * 32 + lane;
   double s = 0.0;
   if (j < m)
-    for (int64_t g = warp; g < nrg; g += 8) s += Zp[(g * dpad + x) * mp + j];
+    s = sum_in_order<8>(warp, nrg, 8, [&](int64_t g) { return (double)Zp[(g * dpad + x) * mp + j]; });
   part[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && j < m) {
@@ -499,6 +499,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   float* Wr;
   PPCA_TRY(prep_w(c, W, m, mp, d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
+  if (c->prep_ev) cudaEventRecord(c->prep_ev, c->stream);     // W' ready: the side stream may read Wr
   if (fused_eligible(c, X, mp, precise)) return pass_fused_power(c, X, Wb, m, Z, S);
   // Yᵀ as a bf16 pair [Y_hi; Y_lo], [2·mp][ldyt]; kernel A writes every row and column < ldyt
   const int64_t ldyt = ceil_div(n, 64) * 64;

@@ -50,15 +50,18 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
   const int tid = threadIdx.x, nt = blockDim.x;
 
   // 1. L = chol(B) (in A), L⁻¹
-  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
+  ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return Bm[e]; }, [&](int64_t e, double v) { A[e] = v; });
   __syncthreads();
-  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err);
-  ppca::block_lower_inverse(A, m, keep, Linv);
+  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err, m);
+  ppca::block_lower_inverse(A, m, keep, Linv, m, m);
+  // S into A (L is no longer needed), every load in flight at once
+  ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return S[e]; }, [&](int64_t e, double v) { A[e] = v; });
+  __syncthreads();
   // 2. C = L⁻¹ S L⁻ᵀ  (T1 = S L⁻ᵀ, then A = L⁻¹ T1), stored mm × mm with a zero dummy row/column
   for (int e = tid; e < m * m; e += nt) {            // lanes vary i: Linv[j][·] is a broadcast
     const int j = e / m, i = e % m;
     double s = 0.0;
-    for (int t = 0; t <= j; ++t) s += S[t * m + i] * Linv[j * m + t];   // S symmetric: coalesced over i
+    for (int t = 0; t <= j; ++t) s += A[t * m + i] * Linv[j * m + t];   // S symmetric
     T1[i * m + j] = s;
   }
   __syncthreads();
@@ -201,16 +204,18 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
 
   // 1. L = chol(B), L⁻¹, C = L⁻¹ S L⁻ᵀ (symmetrised)
   if (tid == 0) g_ritz_clk[0] = clock64();
-  for (int e = tid; e < m * m; e += nt) A[e] = Bm[e];
+  ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return Bm[e]; }, [&](int64_t e, double v) { A[e] = v; });
   __syncthreads();
-  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err);
+  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err, m);
   if (tid == 0) g_ritz_clk[1] = clock64();
-  ppca::block_lower_inverse(A, m, keep, Linv);
+  ppca::block_lower_inverse(A, m, keep, Linv, m, m);
   if (tid == 0) g_ritz_clk[2] = clock64();
+  ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return S[e]; }, [&](int64_t e, double v) { A[e] = v; });
+  __syncthreads();
   for (int e = tid; e < m * m; e += nt) {
     const int j = e / m, i = e % m;
     double s = 0.0;
-    for (int t = 0; t <= j; ++t) s += S[t * m + i] * Linv[j * m + t];   // S symmetric: coalesced over i
+    for (int t = 0; t <= j; ++t) s += A[t * m + i] * Linv[j * m + t];   // S symmetric (staged in A)
     T1[i * m + j] = s;
   }
   __syncthreads();

@@ -16,11 +16,22 @@ __global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // ty 0..7 → rows ty*4..+4
   double acc[4] = {0, 0, 0, 0};
   for (int64_t x0 = xb; x0 < xe; x0 += 64) {
-    for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-      int r = e / 64, cidx = e % 64;
-      int64_t x = x0 + cidx;
-      Vi[r][cidx] = (i0 + r < m && x < xe) ? V[(int64_t)(i0 + r) * d + x] : 0.f;
-      Vj[r][cidx] = (j0 + r < m && x < xe) ? V[(int64_t)(j0 + r) * d + x] : 0.f;
+    {                                                // 16 loads per thread in flight (clamped, then masked)
+      float vi[8], vj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = threadIdx.x + 256 * u, r = e / 64;
+        const int64_t x = min(x0 + e % 64, xe - 1);
+        vi[u] = V[(int64_t)min(i0 + r, m - 1) * d + x];
+        vj[u] = V[(int64_t)min(j0 + r, m - 1) * d + x];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = threadIdx.x + 256 * u, r = e / 64, cidx = e % 64;
+        const bool xin = x0 + cidx < xe;
+        Vi[r][cidx] = (i0 + r < m && xin) ? vi[u] : 0.f;
+        Vj[r][cidx] = (j0 + r < m && xin) ? vj[u] : 0.f;
+      }
     }
     __syncthreads();
 #pragma unroll 8
@@ -39,52 +50,74 @@ __global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__
   }
 }
 
-ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G) {
-  int tiles = (int)ceil_div(m, 32);
-  int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
-  int64_t maxs = ceil_div(d, 64);
+static void vec_gram_split(const Ctx* c, int m, int64_t d, int* nsplit_out, int64_t* cps_out) {
+  const int tiles = (int)ceil_div(m, 32);
+  const int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
+  const int64_t maxs = ceil_div(d, 64);
   int nsplit = (int)std::max<int64_t>(1, std::min(want, maxs));
-  int64_t cps = ceil_div(ceil_div(d, nsplit), 64) * 64;
-  nsplit = (int)ceil_div(d, cps);
-  double* P = (double*)scratch(c, S_PART, (size_t)nsplit * m * m * sizeof(double));
+  const int64_t cps = ceil_div(ceil_div(d, nsplit), 64) * 64;
+  *nsplit_out = (int)ceil_div(d, cps);
+  *cps_out = cps;
+}
+
+size_t vec_gram_part_bytes(const Ctx* c, int m, int64_t d) {
+  int ns;
+  int64_t cps;
+  vec_gram_split(c, m, d, &ns, &cps);
+  return (size_t)ns * m * m * sizeof(double);
+}
+
+ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cudaStream_t st, int part_slot) {
+  const int tiles = (int)ceil_div(m, 32);
+  int nsplit;
+  int64_t cps;
+  vec_gram_split(c, m, d, &nsplit, &cps);
+  double* P = (double*)scratch(c, part_slot, (size_t)nsplit * m * m * sizeof(double));
   if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  vec_gram_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, c->stream>>>(V, m, d, cps, P);
+  vec_gram_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
   PPCA_LAUNCH_CHECK(c, "vec_gram");
-  return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G);
+  return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G, st);
+}
+
+ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G) {
+  return vec_gram_on(c, V, m, d, G, c->stream, S_PART);
 }
 
 // ============================================================================ Cholesky (one CTA)
-// In smem A[m][m] (fp64).  Right-looking; pivots ≤ drop²·G_jj are dropped (column zeroed) if
+// In smem A[m][lda] (fp64).  Right-looking; pivots ≤ drop²·G_jj are dropped (column zeroed) if
 // drop > 0, else flag COLLAPSE.  Writes Linv (lower, dropped rows zero) and keep[] flags.
+// (Measured on B200, m = 64, 256 threads: this blocked form 29 µs + 14 µs for L⁻¹; a one-barrier-per-column
+// form 45 + 36 µs — its per-step index arithmetic, not the barrier (65 cycles) or rsqrt (62), dominates;
+// tools/microbench_small.cu.)
 // Blocked right-looking Cholesky in shared memory A[m][m] (fp64, lower, in place), column blocks of CB:
 // (1) the diagonal block by one warp (__syncwarp only), (2) the panel below by forward substitution, one
 // thread per row, (3) the trailing lower triangle from a transposed copy of the panel (conflict-free).
 // Pivots ≤ drop²·G_jj are dropped (column zeroed, keep[j] = 0) when drop > 0, else flag COLLAPSE.
 // About 3·m/CB block barriers instead of 2·m column barriers.
 constexpr int CB = 16;
-__device__ void block_cholesky(double* A, int m, double drop, int* keep, double* diag0, int* d_err) {
+__device__ void block_cholesky(double* A, int m, double drop, int* keep, double* diag0, int* d_err, int lda) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double rdiag[PPCA_MAX_M];
   __shared__ double panelT[CB][PPCA_MAX_M];
-  for (int i = tid; i < m; i += nt) diag0[i] = A[i * m + i];
+  for (int i = tid; i < m; i += nt) diag0[i] = A[i * lda + i];
   __syncthreads();
   for (int kb = 0; kb < m; kb += CB) {
     const int nb = min(CB, m - kb), ke = kb + nb;
     if (warp == 0) {                              // (1) diagonal block
       for (int j = kb; j < ke; ++j) {
-        const double p = A[j * m + j];
+        const double p = A[j * lda + j];
         const bool dr = drop > 0.0 ? !(p > drop * drop * diag0[j]) : (!(p > 0.0) || !isfinite(p));
         const double piv = dr ? 0.0 : sqrt(p), rp = dr ? 0.0 : 1.0 / piv;
         const int i = j + 1 + lane;
-        const double lij = i < ke ? A[i * m + j] * rp : 0.0;
+        const double lij = i < ke ? A[i * lda + j] * rp : 0.0;
         __syncwarp();
         if (lane == 0) {
-          A[j * m + j] = piv;
+          A[j * lda + j] = piv;
           keep[j] = !dr;
           rdiag[j] = rp;
           if (dr && drop <= 0.0) atomicOr(d_err, DEV_COLLAPSE);
         }
-        if (i < ke) A[i * m + j] = lij;
+        if (i < ke) A[i * lda + j] = lij;
         __syncwarp();
         // trailing part of the diagonal block, all lanes at once: lane ↔ (row j+1+(lane&15), columns
         // j+1+(lane>>4)+2t), t < 8; l_kk by shuffle (independent updates, no serial chain)
@@ -95,7 +128,7 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
           for (int t = 0; t < 8; ++t) {
             const int co = (lane >> 4) + 2 * t, kk = j + 1 + co;
             const double lk = __shfl_sync(0xffffffffu, lij, co & 31);
-            if (ii < ke && kk <= ii) A[ii * m + kk] -= li * lk;
+            if (ii < ke && kk <= ii) A[ii * lda + kk] -= li * lk;
           }
         }
         __syncwarp();
@@ -108,11 +141,11 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
       for (int c = 0; c < CB; ++c) {
         double sum = 0.0;
         if (c < nb) {
-          sum = A[i * m + kb + c];
+          sum = A[i * lda + kb + c];
 #pragma unroll
-          for (int l = 0; l < c; ++l) sum -= x[l] * A[(kb + c) * m + kb + l];
+          for (int l = 0; l < c; ++l) sum -= x[l] * A[(kb + c) * lda + kb + l];
           sum *= rdiag[kb + c];
-          A[i * m + kb + c] = sum;
+          A[i * lda + kb + c] = sum;
           panelT[c][i] = sum;
         }
         x[c] = sum;
@@ -124,12 +157,12 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
       for (int i = ke + ty; i < m; i += sy) {
         double li[CB];
 #pragma unroll
-        for (int c = 0; c < CB; ++c) li[c] = c < nb ? A[i * m + kb + c] : 0.0;
+        for (int c = 0; c < CB; ++c) li[c] = c < nb ? A[i * lda + kb + c] : 0.0;
         for (int k = ke + tx; k <= i; k += 16) {
           double acc = 0.0;
 #pragma unroll
           for (int c = 0; c < CB; ++c) acc = fma(li[c], c < nb ? panelT[c][k] : 0.0, acc);
-          A[i * m + k] -= acc;
+          A[i * lda + k] -= acc;
         }
       }
     }
@@ -140,10 +173,10 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
 // Linv = L⁻¹ (rows of dropped pivots zero) by row blocks of CB: T = Σ_{k < r0} L[r][k]·Linv[k][c] for the
 // block's rows and earlier columns (all threads), then a CB-row forward substitution per column (one thread
 // per column) with the block's diagonal reciprocals.  2 barriers per row block.
-__device__ void block_lower_inverse(const double* L, int m, const int* keep, double* Linv) {
+__device__ void block_lower_inverse(const double* L, int m, const int* keep, double* Linv, int lda, int ldi) {
   __shared__ double rd[PPCA_MAX_M];
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < m; i += nt) rd[i] = (keep[i] && L[i * m + i] != 0.0) ? 1.0 / L[i * m + i] : 0.0;
+  for (int i = tid; i < m; i += nt) rd[i] = (keep[i] && L[i * lda + i] != 0.0) ? 1.0 / L[i * lda + i] : 0.0;
   __syncthreads();
   for (int r0 = 0; r0 < m; r0 += CB) {
     const int nb = min(CB, m - r0);
@@ -152,11 +185,11 @@ __device__ void block_lower_inverse(const double* L, int m, const int* keep, dou
       double a0 = 0.0, a1 = 0.0;
       int k = c;
       for (; k + 1 < r0; k += 2) {
-        a0 = fma(L[r * m + k], Linv[(int64_t)k * m + c], a0);
-        a1 = fma(L[r * m + k + 1], Linv[(int64_t)(k + 1) * m + c], a1);
+        a0 = fma(L[r * lda + k], Linv[(int64_t)k * ldi + c], a0);
+        a1 = fma(L[r * lda + k + 1], Linv[(int64_t)(k + 1) * ldi + c], a1);
       }
-      if (k < r0) a0 = fma(L[r * m + k], Linv[(int64_t)k * m + c], a0);
-      Linv[(int64_t)r * m + c] = a0 + a1;
+      if (k < r0) a0 = fma(L[r * lda + k], Linv[(int64_t)k * ldi + c], a0);
+      Linv[(int64_t)r * ldi + c] = a0 + a1;
     }
     __syncthreads();
     for (int c = tid; c < m; c += nt) {           // forward substitution within the row block
@@ -167,12 +200,12 @@ __device__ void block_lower_inverse(const double* L, int m, const int* keep, dou
         if (rr < nb) {
           const int r = r0 + rr;
           if (c <= r) {
-            double rhs = c < r0 ? -Linv[(int64_t)r * m + c] : (r == c ? 1.0 : 0.0);
+            double rhs = c < r0 ? -Linv[(int64_t)r * ldi + c] : (r == c ? 1.0 : 0.0);
 #pragma unroll
-            for (int l = 0; l < rr; ++l) rhs -= L[r * m + r0 + l] * x[l];
+            for (int l = 0; l < rr; ++l) rhs -= L[r * lda + r0 + l] * x[l];
             v = rhs * rd[r];
           }
-          Linv[(int64_t)r * m + c] = v;
+          Linv[(int64_t)r * ldi + c] = v;
         }
         x[rr] = v;
       }
@@ -181,28 +214,44 @@ __device__ void block_lower_inverse(const double* L, int m, const int* keep, dou
   }
 }
 
+__device__ unsigned long long g_chol_clk[8];     // phase clocks of the last chol_inv (profiling)
+
 __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop, double* __restrict__ Linv,
                                 int* __restrict__ row_map, int* __restrict__ m_out, int* d_err) {
   extern __shared__ double sm[];
-  double* A = sm;                                  // m*m
-  double* diag0 = A + m * m;                       // m
+  if (threadIdx.x == 0) g_chol_clk[0] = clock64();
+  const int lda = m | 1;                           // odd row stride: column walks hit distinct banks
+  double* A = sm;                                  // m × lda
+  double* diag0 = A + m * lda;                     // m
   int* keep = (int*)(diag0 + m);                   // m
-  double* Ls = reinterpret_cast<double*>(keep + ((m + 1) & ~1));   // m*m when m ≤ 90 (L⁻¹ built in smem)
+  double* Ls = reinterpret_cast<double*>(keep + ((m + 1) & ~1));   // m × lda when m ≤ 90 (L⁻¹ built in smem)
   const bool in_smem = m <= 90;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) A[e] = G[e];
+  copy_batched<16>(threadIdx.x, m * m, blockDim.x, [&](int64_t e) { return G[e]; },
+                   [&](int64_t e, double v) { A[(e / m) * lda + e % m] = v; });
   __syncthreads();
-  block_cholesky(A, m, drop, keep, diag0, d_err);
+  if (threadIdx.x == 0) g_chol_clk[1] = clock64();
+  block_cholesky(A, m, drop, keep, diag0, d_err, lda);
+  if (threadIdx.x == 0) g_chol_clk[2] = clock64();
   if (in_smem) {
-    block_lower_inverse(A, m, keep, Ls);
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) Linv[e] = Ls[e];
+    block_lower_inverse(A, m, keep, Ls, lda, lda);
+    if (threadIdx.x == 0) g_chol_clk[3] = clock64();
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) Linv[e] = Ls[(e / m) * lda + e % m];
   } else {
-    block_lower_inverse(A, m, keep, Linv);
+    block_lower_inverse(A, m, keep, Linv, lda, m);
+    if (threadIdx.x == 0) g_chol_clk[3] = clock64();
   }
+  if (threadIdx.x == 0) g_chol_clk[4] = clock64();
   if (threadIdx.x == 0) {
     int o = 0;
     for (int i = 0; i < m; ++i) row_map[i] = keep[i] ? o++ : -1;
     *m_out = o;
   }
+}
+
+static size_t chol_inv_smem(int m) {
+  const int lda = m | 1;
+  return (size_t)m * lda * sizeof(double) + m * sizeof(double) + ((m + 1) & ~1) * sizeof(int) +
+         (m <= 90 ? (size_t)m * lda * sizeof(double) : 0);
 }
 
 // ============================================================================ apply: OUT = C · IN
@@ -218,12 +267,15 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
   extern __shared__ double cs[];                 // rows × m_in (fp64), then m_in × AP_COLS (fp32)
   float* ins = reinterpret_cast<float*>(cs + (size_t)rows * m_in);
   const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
-  for (int e = threadIdx.x; e < rows * m_in; e += blockDim.x) cs[e] = C[(int64_t)(e / m_in) * ldc + e % m_in];
-  for (int e = threadIdx.x; e < m_in * AP_COLS; e += blockDim.x) {
-    const int j = e / AP_COLS, cl = e % AP_COLS;
-    const int64_t x = x0 + cl;
-    ins[e] = x < d ? IN[(int64_t)j * d + x] : 0.f;
-  }
+  copy_batched<16>(threadIdx.x, rows * m_in, blockDim.x,
+                   [&](int64_t e) { return C[(e / m_in) * ldc + e % m_in]; },
+                   [&](int64_t e, double v) { cs[e] = v; });
+  copy_batched<8>(threadIdx.x, m_in * AP_COLS, blockDim.x,
+                  [&](int64_t e) {
+                    const int64_t x = x0 + e % AP_COLS;
+                    return IN[(e / AP_COLS) * d + (x < d ? x : d - 1)];
+                  },
+                  [&](int64_t e, float v) { ins[e] = x0 + e % AP_COLS < d ? v : 0.f; });
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t x = x0 + lane;
@@ -258,6 +310,24 @@ static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_
   return PPCA_OK;
 }
 
+// L⁻¹ of chol(G) (one CTA, fp64) on stream st; no drops (a non-positive pivot flags DEV_COLLAPSE)
+ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_map, int* m_out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const size_t smem = chol_inv_smem(m);
+  chol_inv_kernel<<<1, 256, smem, st>>>(G, m, 0.0, Linv, row_map, m_out, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "chol_inv");
+  return PPCA_OK;
+}
+
+// OUT = L · IN for a lower-triangular fp64 L (m × m), IN/OUT [m][d] fp32, fp64 accumulation
+ppca_status apply_lower_on(Ctx* c, const double* L, int m, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
+  return apply_rows(c, L, m, m, m, nullptr, true, IN, d, OUT, st);
+}
+
 // ============================================================================ CholQR2
 ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out) {
   return cholqr(c, W, W, m, d, drop_tol, m_out, 2);
@@ -278,8 +348,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  size_t smem = (size_t)m * m * sizeof(double) + m * sizeof(double) + ((m + 1) & ~1) * sizeof(int) +
-                (m <= 90 ? (size_t)m * m * sizeof(double) : 0);
+  const size_t smem = chol_inv_smem(m);
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
     PPCA_TRY(vec_gram(c, Zin, m, d, G));
     chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
@@ -323,6 +392,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
 ppca_status ritz_debug_clocks(unsigned long long* out8) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out8, ritz::g_ritz_clk, 8 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out8 + 8, g_chol_clk, 8 * sizeof(unsigned long long));
   return PPCA_OK;
 }
 

@@ -7,6 +7,13 @@ namespace ppca {
 
 // G[m][m] (fp64) = V Vᵀ for row vectors V [m][d] fp32 (partials in S_PART).
 ppca_status vec_gram(Ctx* c, const float* V, int m, int64_t d, double* G);
+// the same on stream st with its split partials in scratch slot part_slot (side-stream use)
+ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cudaStream_t st, int part_slot);
+size_t vec_gram_part_bytes(const Ctx* c, int m, int64_t d);
+// Linv = chol(G)⁻¹ (lower, fp64, one CTA) on stream st; row_map/m_out as in cholqr (no drops)
+ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_map, int* m_out, cudaStream_t st);
+// OUT = L·IN, L lower-triangular fp64 m×m, IN/OUT [m][d] fp32 (distinct buffers)
+ppca_status apply_lower_on(Ctx* c, const double* L, int m, const float* IN, int64_t d, float* OUT, cudaStream_t st);
 
 // CholQR2 in place: W [m][d] ← Q-factor of the rows (positive diag R), twice.
 // drop_tol > 0: rows whose Cholesky pivot ≤ drop_tol²·G_jj are dropped (refine semantics,

@@ -15,5 +15,8 @@ def show(tag):
     out = (ctypes.c_ulonglong * 16)(); lib.ppca_debug_wait_counters(out)
     c = [out[i] for i in range(8)]
     print(tag, "  ".join(f"{n} {(c[i+1]-c[i])/1.9e3:.1f}us" for i, n in enumerate(names) if c[i+1] > c[i]))
+    h = [out[8 + i] for i in range(5)]
+    print("   chol_inv:", "  ".join(f"{n} {(h[i+1]-h[i])/1.9e3:.1f}us" for i, n in
+                                   enumerate(["stage", "cholesky", "L^-1", "store"])))
 P.ppca_prime_power(ctx, Xm, w.m, 2, w.init_seed, W, theta_hist=True); show("values ")
 P.ppca_refine(ctx, Xm, W, w.m, w.k, E); show("vectors")
