@@ -203,11 +203,11 @@ static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& 
   return PPCA_OK;
 }
 
-template <int MP, bool XBF16, bool XLO>
+template <int MP, bool XBF16, bool XLO, bool LEAN>
 static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
                              const KBParams& bp, int grid) {
-  const size_t smem = kb::Cfg<MP, XLO>::SMEM;
-  auto kern = xty_tc_kernel<MP, XBF16, XLO>;
+  const size_t smem = kb::Cfg<MP, XLO, LEAN>::SMEM;
+  auto kern = xty_tc_kernel<MP, XBF16, XLO, LEAN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, kb::NTHREADS, smem, c->stream>>>(tmYT, tmX, tmXlo, bp);
   PPCA_LAUNCH_CHECK(c, "xty_tc_kernel");
@@ -257,18 +257,18 @@ static ppca_status dispatch_ka(Ctx* c, int mp, const CUtensorMap& tmW, const CUt
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
 
-template <bool XBF16, bool XLO>
+template <bool XBF16, bool XLO, bool LEAN = false>
 static ppca_status dispatch_kb(Ctx* c, int mp, const CUtensorMap& tmYT, const CUtensorMap& tmX,
                                const CUtensorMap& tmXlo, const KBParams& bp, int grid) {
   switch (mp) {
-    case 16: return launch_kb<16, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 32: return launch_kb<32, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 48: return launch_kb<48, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 64: return launch_kb<64, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 80: return launch_kb<80, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 96: return launch_kb<96, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 112: return launch_kb<112, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
-    case 128: return launch_kb<128, XBF16, XLO>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 16: return launch_kb<16, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 32: return launch_kb<32, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 48: return launch_kb<48, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 64: return launch_kb<64, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 80: return launch_kb<80, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 96: return launch_kb<96, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 112: return launch_kb<112, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
+    case 128: return launch_kb<128, XBF16, XLO, LEAN>(c, tmYT, tmX, tmXlo, bp, grid);
   }
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
@@ -497,10 +497,13 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   const int64_t n = X->n_local, d = X->d;
   __nv_bfloat16* Wb;
   float* Wr;
+  const bool fused = fused_eligible(c, X, mp, precise);
+  // bf16 X outside the fused kernel and outside the minibatch steps: product 2 with Y_hi alone (R27)
+  const bool lean = X->dtype == PPCA_BF16 && !fused && !precise;
   PPCA_TRY(prep_w(c, W, m, mp, d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
   if (c->prep_ev) cudaEventRecord(c->prep_ev, c->stream);     // W' ready: the side stream may read Wr
-  if (fused_eligible(c, X, mp, precise)) return pass_fused_power(c, X, Wb, m, Z, S);
+  if (fused) return pass_fused_power(c, X, Wb, m, Z, S);
   // Yᵀ as a bf16 pair [Y_hi; Y_lo], [2·mp][ldyt]; kernel A writes every row and column < ldyt
   const int64_t ldyt = ceil_div(n, 64) * 64;
   __nv_bfloat16* YT = (__nv_bfloat16*)scratch(c, S_Y, (size_t)2 * mp * ldyt * 2);
@@ -545,7 +548,8 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   if (!Zp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   bp.Zp = Zp;
   CUtensorMap tmYT, tmX, tmXlo;
-  if (!make_map_bf16(&tmYT, YT, ldyt, 2 * mp, ldyt, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map YT failed");
+  const int yrows = lean ? mp : 2 * mp;
+  if (!make_map_bf16(&tmYT, YT, ldyt, yrows, ldyt, yrows)) return set_error(c, PPCA_ERR_CUDA, "tensor map YT failed");
   tmX = tmYT;
   // product 2 reads X_hi only: bf16 X, or the hi plane of a split X, by TMA
   if (X->dtype != PPCA_F32 && !make_x_maps(X, kb::KR, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
@@ -555,6 +559,8 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
     PPCA_TRY((dispatch_kb<false, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   else if (precise && X->dtype == PPCA_F32_SPLIT)
     PPCA_TRY((dispatch_kb<true, true>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
+  else if (lean)
+    PPCA_TRY((dispatch_kb<true, false, true>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   else
     PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   kernel_timer_mark(c, 1);

@@ -18,11 +18,11 @@ constexpr int NTHREADS = 14 * 32;
 constexpr uint32_t BLK = KR * 128;            // one 64-column block of a stage (bytes)
 // XLO: the X_lo plane of a split X is staged too and X_loᵀ·Y_hi is added (the minibatch steps, whose
 // products are the update itself; the power pass reads X_hi only)
-template <int MP, bool XLO = false> struct Cfg {
+template <int MP, bool XLO = false, bool LEAN = false> struct Cfg {
   // 256-column d-groups for every m: the Yᵀ operand (2·MP rows per 64-row stage) is then streamed from L2 once
   // per 256 X columns (C5, MP = 128: with 128-column groups Yᵀ moved twice X's bytes through L2)
   static constexpr int NC = 2;                            // 128-wide d chunks per work item
-  static constexpr int NB = 2 * MP;                      // UMMA N: [Y_hi; Y_lo]
+  static constexpr int NB = LEAN ? MP : 2 * MP;          // UMMA N: [Y_hi; Y_lo] (Y_hi alone: bf16 X, R27)
   static constexpr uint32_t XST = NC * 2 * BLK;          // X stage bytes (one plane)
   static constexpr uint32_t XSTG = XLO ? 2 * XST : XST;  // X stage bytes (all planes)
   static constexpr uint32_t YST = NB * 128;              // Yᵀ stage bytes (NB rows × 64 K)
@@ -45,12 +45,12 @@ struct KBParams {
   float* Zp;                // [nrg][d_pad][mp] fp32 partials (d_pad = ndg·NC·128)
 };
 
-template <int MP, bool XBF16, bool XLO = false>
+template <int MP, bool XBF16, bool XLO = false, bool LEAN = false>
 __global__ void __launch_bounds__(kb::NTHREADS, 1)
     xty_tc_kernel(const __grid_constant__ CUtensorMap tmYT, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, KBParams p) {
   using namespace kb;
-  using CF = Cfg<MP, XLO>;
+  using CF = Cfg<MP, XLO, LEAN>;
   constexpr int NC = CF::NC, NB = CF::NB, NST = CF::NSTG, NBUF = CF::NBUF;
   constexpr uint32_t XST = CF::XSTG, XPL = CF::XST, YST = CF::YST, ACC = CF::ACC, TCOLS = CF::TCOLS;
   static_assert(!XLO || XBF16, "the X_lo plane is staged by TMA");
@@ -268,9 +268,9 @@ __global__ void __launch_bounds__(kb::NTHREADS, 1)
           float v[16], w[16];
           const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + b * ACC + c * NB + c0;
           tmem_ld16(ta, v);
-          tmem_ld16(ta + MP, w);
+          if (!LEAN) tmem_ld16(ta + MP, w);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = nks == 0 ? 0.f : v[j] + w[j];
+          for (int j = 0; j < 16; ++j) v[j] = nks == 0 ? 0.f : (LEAN ? v[j] : v[j] + w[j]);
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
             *reinterpret_cast<float4*>(out + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
