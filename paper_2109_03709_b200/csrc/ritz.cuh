@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
 // per round).  O(m³/nt + m²) instead of Jacobi's O(sweeps·m) barrier rounds.
 //
 // With R != nullptr (m ≤ 64: the refine) the eigenvectors follow too: inverse iteration on the tridiagonal
-// (Gaussian elimination with partial pivoting, 3 steps, clusters of eigenvalues closer than 1e-3·‖T‖ handled
+// (Gaussian elimination with partial pivoting, 3 steps, clusters of eigenvalues closer than 1e-9·‖T‖ handled
 // by one thread with Gram–Schmidt against the cluster's earlier vectors at every step), back-transformation
 // by the stored Householder reflectors (one thread per vector), then R = Uᵀ L⁻¹ in descending order.
 __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
@@ -357,7 +357,11 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   if (!vectors) return;
   // 4. eigenvectors of T: inverse iteration, one thread per cluster of close eigenvalues
   double* XT = T1;                                    // XT[i·m + j] = component i of eigenvector j (ascending)
-  const double ctol = 1e-3 * fmax(fabs(lo), fabs(hi));
+  // clusters: gaps ≤ 1e-9·‖T‖.  Inverse iteration separates eigenvalues whose gap δ exceeds the shifts'
+  // error (~ε‖T‖) and leaves the vectors orthogonal to ~ε‖T‖/δ ≤ 2e-7 here (below the fp32 outputs'
+  // rounding); LAPACK's 1e-3·‖T‖ would put most of a power-law spectrum (C4: gaps 1.5·j^-2.5·λ₁) into
+  // one serial Gram–Schmidt chain (8.5 ms per refine, measured)
+  const double ctol = 1e-9 * fmax(fabs(lo), fabs(hi));
   const double tiny = 1e-14 * span;
   for (int j0 = tid; j0 < m; j0 += nt) {
     if (j0 > 0 && evals[j0] - evals[j0 - 1] <= ctol) continue;   // not a cluster leader
