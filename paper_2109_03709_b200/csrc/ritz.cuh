@@ -428,19 +428,32 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   }
   __syncthreads();
   if (tid == 0) g_ritz_clk[6] = clock64();
-  // 5. back-transformation y = H_0 ⋯ H_{m-3} x (one thread per vector; reflector reads are broadcasts)
-  for (int j = tid; j < m; j += nt) {
+  // 5. back-transformation y = H_0 ⋯ H_{m-3} x.  Thread (j, s): lane-consecutive vectors j (conflict-free
+  //    XT columns, reflector entries broadcast), s = one of nt/64 row slices; per reflector the slices'
+  //    partial dot products meet in shared memory (two barriers per reflector)
+  {
+    const int ns = nt / 64 < 1 ? 1 : (nt / 64 > 8 ? 8 : nt / 64);
+    const int j = tid % 64, sl = tid / 64;
+    const bool own = j < m && sl < ns;
+    __shared__ double red[8 * 64];                    // ns × 64 partial dots
     for (int k = m - 3; k >= 0; --k) {
       const double bk = hbeta[k];
       if (bk == 0.0) continue;
       const int n1 = m - k - 1;
       double dt = 0.0;
-      for (int i = 0; i < n1; ++i) dt += A[(k + 1 + i) * m + k] * XT[(k + 1 + i) * m + j];
-      dt *= bk;
-      for (int i = 0; i < n1; ++i) XT[(k + 1 + i) * m + j] -= dt * A[(k + 1 + i) * m + k];
+      if (own)
+        for (int i = sl; i < n1; i += ns) dt += A[(k + 1 + i) * m + k] * XT[(k + 1 + i) * m + j];
+      if (own) red[sl * 64 + j] = dt;
+      __syncthreads();
+      if (own) {
+        double tot = 0.0;
+        for (int q = 0; q < ns; ++q) tot += red[q * 64 + j];
+        tot *= bk;
+        for (int i = sl; i < n1; i += ns) XT[(k + 1 + i) * m + j] -= tot * A[(k + 1 + i) * m + k];
+      }
+      __syncthreads();
     }
   }
-  __syncthreads();
   if (tid == 0) g_ritz_clk[7] = clock64();
   // 6. R = Uᵀ L⁻¹ in descending order (row i ↔ ascending eigenvector m-1-i)
   for (int e = tid; e < m * m; e += nt) {
