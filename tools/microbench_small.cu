@@ -119,6 +119,63 @@ __global__ void k_step2(int iters, unsigned long long* out, double* sink) {
   if (threadIdx.x == 0) { out[6] = (t1 - t0) / iters; sink[5] = A[5]; }
 }
 
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// one Householder tridiagonalisation sweep (m = 64) as in ritz_values_kernel; which = 0 full step,
+// 1 without the matvec, 2 without the rank-2 update, 3 only barriers + reductions
+__global__ void k_tridiag(int which, unsigned long long* out, double* sink) {
+  extern __shared__ double A[];
+  __shared__ double vec[128], pv[128];
+  const int m = 64, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+  for (int i = tid; i < m * m; i += nt) A[i] = ((i / m) == (i % m) ? 2.0 : 0.0) + 1.0 / (1 + (i / m) + (i % m));
+  __syncthreads();
+  long long t0 = clock64();
+  for (int k = 0; k + 2 < m; ++k) {
+    const int n1 = m - k - 1;
+    const double* col = A + (k + 1) * m + k;
+    double ss = 0.0;
+    for (int i = lane; i < n1; i += 32) ss += col[i * m] * col[i * m];
+    ss = wsum(ss);
+    const double x0 = col[0];
+    const double alpha = ss > 0.0 ? -copysign(sqrt(ss), x0) : 0.0;
+    const double v0 = x0 - alpha;
+    const double vtv = ss - x0 * x0 + v0 * v0;
+    const double beta = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    const double vi = tid < n1 ? (tid == 0 ? col[0] - alpha : col[tid * m]) : 0.0;
+    __syncthreads();
+    if (tid < n1) vec[tid] = vi;
+    __syncthreads();
+    if (which != 1 && which != 3) {
+      for (int i = warp; i < n1; i += nw) {
+        const double* row = A + (k + 1 + i) * m + (k + 1);
+        double acc = 0.0;
+        for (int j = lane; j < n1; j += 32) acc = fma(row[j], vec[j], acc);
+        acc = wsum(acc);
+        if (lane == 0) pv[i] = beta * acc;
+      }
+    }
+    __syncthreads();
+    double kk = 0.0;
+    for (int i = lane; i < n1; i += 32) kk += vec[i] * pv[i];
+    kk = wsum(kk);
+    const double K = 0.5 * beta * kk;
+    if (which != 2 && which != 3) {
+      for (int i = warp; i < n1; i += nw) {
+        const double vv = vec[i], ww = pv[i] - K * vv;
+        double* Ai = A + (k + 1 + i) * m + (k + 1);
+        for (int j = lane; j < n1; j += 32) Ai[j] -= vv * (pv[j] - K * vec[j]) + ww * vec[j];
+      }
+    }
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (tid == 0) { out[7 + which] = (t1 - t0) / 62; sink[6] = A[7]; }
+}
+
 int main() {
   unsigned long long* out;
   double* sink;
@@ -133,10 +190,13 @@ int main() {
     k_smem_chain<<<1, 256>>>(1000, out, sink);
     k_step<<<1, 256>>>(1000, out, sink);
     k_step2<<<1, 256>>>(1000, out, sink);
+    for (int w = 0; w < 4; ++w) k_tridiag<<<1, 512, 64 * 64 * 8>>>(w, out, sink);
   }
   unsigned long long h[16];
   cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
   printf("cycles per iteration: syncthreads(256) %llu  rsqrt(f64) %llu  1/sqrt(f64) %llu  dfma %llu  smem RMW %llu  "
          "chol-step %llu  batched %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+  printf("tridiag step cycles (512 thr): full %llu  no-matvec %llu  no-update %llu  sync+reductions %llu\n", h[7], h[8],
+         h[9], h[10]);
   return 0;
 }
