@@ -160,24 +160,41 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
 // ============================================================================ kernel B (tc_xty.cuh)
 #include "tc_xty.cuh"
 
-// Z[j][x] = Σ_g Zp[g][x][j]   (fixed order over row groups)
-// Block (x, 32 consecutive j): lanes read 128 contiguous bytes of a partial row; warp w sums row groups
-// g ≡ w (mod 8); the 8 warp sums are added in warp order (deterministic).
+// Z[j][x] = Σ_g Zp[g][x][j], g in order (fixed, deterministic).  Block = ZP_XB columns × all mp features:
+// the block's slice of each partial is ZP_XB·mp contiguous floats, read coalesced, with the partials of
+// 8 row groups in flight per thread; the sums leave through shared memory as ZP_XB-float runs of Z's rows.
+constexpr int ZP_XB = 8;
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z) {
-  __shared__ double part[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t x = blockIdx.x;
-  const int j = blockIdx.y * 32 + lane;
-  double s = 0.0;
-  if (j < m)
-    s = sum_in_order<8>(warp, nrg, 8, [&](int64_t g) { return (double)Zp[(g * dpad + x) * mp + j]; });
-  part[warp][lane] = s;
+  __shared__ float tr[128][ZP_XB + 1];
+  const int64_t x0 = (int64_t)blockIdx.x * ZP_XB;
+  const int cnt = ZP_XB * mp;                        // ≤ 1024: ≤ 4 elements per thread
+  const float* base = Zp + x0 * mp;
+  const int64_t gstride = dpad * mp;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t g0 = 0; g0 < nrg; g0 += 8) {
+    float v[8][4];
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = threadIdx.x + 256 * u;
+        v[gg][u] = (g0 + gg < nrg && e < cnt) ? base[(g0 + gg) * gstride + e] : 0.f;
+      }
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += (double)v[gg][u];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = threadIdx.x + 256 * u;
+    if (e < cnt) tr[e % mp][e / mp] = (float)acc[u];
+  }
   __syncthreads();
-  if (warp == 0 && j < m) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += part[w][lane];
-    Z[(int64_t)j * d + x] = (float)t;
+  for (int e = threadIdx.x; e < m * ZP_XB; e += 256) {
+    const int j = e / ZP_XB, xl = e % ZP_XB;
+    if (x0 + xl < d) Z[(int64_t)j * d + x0 + xl] = tr[j][xl];
   }
 }
 
@@ -486,7 +503,7 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   kernel_timer_mark(c, 0);
   reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
-  reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+  reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
 }
@@ -564,7 +581,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   else
     PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   kernel_timer_mark(c, 1);
-  reduce_zp_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
+  reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
 }
