@@ -1,4 +1,6 @@
 // small.cu — m×m side of the hot path (see small.cuh).  All m×m arithmetic is fp64.
+#include <cooperative_groups.h>
+
 #include "small.cuh"
 #include "gemm_simt.cuh"
 
@@ -601,8 +603,187 @@ __global__ void eg_elementwise_kernel(const float* __restrict__ MV, const float*
   V[e] = (float)w;
 }
 
+// The whole EigenGame update in ONE cooperative kernel (the 5-launch sequence above costs ≈ 37 µs per C4 step,
+// latency-bound): every CTA forms Cf and 2U from A itself (m×m, in shared memory — no barrier needed), then
+// per 32-column chunk (lane = column, warp = rows j ≡ w mod 8): T_j = Σ_{i<j} Cf_ji·MV_i from a staged MV slab,
+// r, Nesterov, V (unnormalised, rounded to fp32 as stored) and this chunk's Σ_x V_jx² per row; one grid
+// barrier; then every CTA sums the chunks' row partials in chunk order (identical in all CTAs) and rescales
+// its columns.  Same arithmetic as eg_coeff + apply_rows + eg_elementwise + normalize_rows.
+constexpr int EG_XC = 32;
+__global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict__ MV, const double* __restrict__ A,
+                                                        float* __restrict__ V, float* __restrict__ vel, int m,
+                                                        int64_t d, double alpha, double mu,
+                                                        double* __restrict__ rowpart, int* d_err) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double egs[];
+  double* Cf = egs;                                   // m × m
+  double* twoU = Cf + (size_t)m * m;                  // m
+  double* rdiag = twoU + m;                           // m
+  double* nrm = rdiag + m;                            // m (reciprocal row norms)
+  float* mvs = reinterpret_cast<float*>(nrm + m);     // m × EG_XC
+  __shared__ double amax;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int64_t nchunks = (d + EG_XC - 1) / EG_XC;
+  // coefficients (eg_coeff_kernel's arithmetic)
+  if (warp == 0) {
+    double mx = 0.0;
+    for (int i = lane; i < m; i += 32) mx = fmax(mx, A[i * m + i]);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) amax = mx;
+  }
+  copy_batched<16>(tid, (int64_t)m * m, blockDim.x, [&](int64_t e) { return A[e]; },
+                   [&](int64_t e, double v) { Cf[e] = v; });
+  __syncthreads();
+  for (int i = tid; i < m; i += blockDim.x) {
+    double aii = Cf[i * m + i];
+    if (!(aii > 1e-12 * amax)) {
+      if (blockIdx.x == 0) atomicOr(d_err, DEV_DEGENERATE);
+      aii = 1.0;
+    }
+    rdiag[i] = 1.0 / aii;
+  }
+  __syncthreads();
+  for (int j = warp; j < m; j += nw) {                // rows j: read A_j· (still in Cf), then overwrite with Cf_j·
+    double part = 0.0;
+    double cfv[PPCA_MAX_M / 32];
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 32; ++q) {
+      const int i = lane + 32 * q;
+      double cf = 0.0;
+      if (i < m && i < j) {
+        const double aji = Cf[j * m + i];
+        cf = aji * rdiag[i];
+        part += aji * cf;
+      }
+      cfv[q] = cf;
+    }
+    part = warp_sum(part);
+    const double ajj = Cf[j * m + j];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 32; ++q) {
+      const int i = lane + 32 * q;
+      if (i < m) Cf[j * m + i] = cfv[q];
+    }
+    if (lane == 0) twoU[j] = 2.0 * (ajj - part);
+  }
+  __syncthreads();
+  // update per column chunk
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t x0 = ch * EG_XC;
+    copy_batched<8>(tid, (int64_t)m * EG_XC, blockDim.x,
+                    [&](int64_t e) {
+                      const int64_t x = x0 + e % EG_XC;
+                      return MV[(e / EG_XC) * d + (x < d ? x : d - 1)];
+                    },
+                    [&](int64_t e, float v) { mvs[e] = v; });
+    __syncthreads();
+    const int64_t x = x0 + lane;
+    for (int j = warp; j < m; j += nw) {
+      const double* cj = Cf + j * m;
+      double t0 = 0.0, t1 = 0.0;
+      int i = 0;
+      for (; i + 1 < j; i += 2) {
+        t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
+        t1 = fma(cj[i + 1], (double)mvs[(i + 1) * EG_XC + lane], t1);
+      }
+      if (i < j) t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
+      const float tf = (float)(t0 + t1);               // T as the apply kernel stores it (fp32)
+      double sq = 0.0;
+      if (x < d) {
+        const int64_t e = (int64_t)j * d + x;
+        const double r = 2.0 * (double)mvs[j * EG_XC + lane] - 2.0 * (double)tf - twoU[j] * (double)V[e];
+        const double v = mu * (double)vel[e] + r;
+        const double w = (double)V[e] + alpha * (r + mu * v);
+        if (!isfinite(w)) atomicOr(d_err, DEV_NONFINITE);
+        vel[e] = (float)v;
+        const float wf = (float)w;
+        V[e] = wf;
+        sq = (double)wf * wf;
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) rowpart[ch * m + j] = sq;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  // row norms: Σ over chunks in chunk order (every CTA the same sums), then rescale this CTA's columns
+  for (int j = warp; j < m; j += nw) {
+    double s2 = 0.0;
+    for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
+      const int64_t c1 = c0 + lane;
+      double v = c1 < nchunks ? rowpart[c1 * m + j] : 0.0;
+      // fixed-order combination inside the warp (lane order), then across the 32-chunk blocks in order
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_down_sync(0xffffffffu, v, o);
+        if ((lane & (2 * o - 1)) == 0) v += u;
+      }
+      s2 += __shfl_sync(0xffffffffu, v, 0);
+    }
+    const double n = sqrt(s2);
+    if (lane == 0) {
+      if (!(n > 1e-300)) {
+        if (blockIdx.x == 0) atomicOr(d_err, DEV_DEGENERATE);
+        nrm[j] = 0.0;
+      } else {
+        nrm[j] = 1.0 / n;
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t x = ch * EG_XC + lane;
+    if (x < d)
+      for (int j = warp; j < m; j += nw) {
+        const int64_t e = (int64_t)j * d + x;
+        if (nrm[j] > 0.0) {
+          const double v = (double)V[e] * nrm[j];
+          if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
+          V[e] = (float)v;
+        }
+      }
+  }
+}
+
+static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
+                                   double alpha, double mu, ppca_status* st) {
+  *st = PPCA_OK;
+  const int64_t nchunks = ceil_div(d, (int64_t)EG_XC);
+  const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) + (size_t)m * EG_XC * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(eg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  int per_sm = 0;
+  if (smem > 200 * 1024 ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eg_update_kernel, 256, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  double* rowpart = (double*)scratch(c, S_ROWRED, (size_t)nchunks * m * sizeof(double));
+  if (!rowpart) {
+    *st = set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    return true;
+  }
+  const int grid = (int)std::min<int64_t>(nchunks, (int64_t)per_sm * c->sm_count);
+  void* args[] = {(void*)&MV, (void*)&A, (void*)&V, (void*)&vel, (void*)&m, (void*)&d, (void*)&alpha, (void*)&mu,
+                  (void*)&rowpart, (void*)&c->d_err};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)eg_update_kernel, grid, 256, args, smem, c->stream);
+  ++c->launches;
+  if (e != cudaSuccess) *st = check_cuda(c, e, "eg_update_kernel");
+  return true;
+}
+
 ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
                              double alpha, double mu) {
+  static int multi = -1;                          // PPCA_EG_MULTI=1: the 5-launch sequence (comparison)
+  if (multi < 0) multi = getenv("PPCA_EG_MULTI") ? atoi(getenv("PPCA_EG_MULTI")) : 0;
+  if (!multi) {
+    ppca_status st;
+    if (eigengame_update_fused(c, MV, A, V, vel, m, d, alpha, mu, &st)) return st;
+  }
   double* Cf = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + (size_t)m * sizeof(double) + 64);
   double* twoU = Cf + (size_t)m * m;
   float* T = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
