@@ -49,6 +49,8 @@ struct KFParams {
   int pf;                        // A-stream L2 prefetch distance in chunks (0 = off)
   int dbg;                       // experiment switches (PPCA_DBG; 0 in production): 1 skip B-stream
   int hi_policy;                 // L2 policy of the A-stream's hi plane: 0 evict_last, 1 normal, 2 evict_first
+  int lag;                       // > 0: the A-stream starts round ρ only once the B-stream finished round ρ−lag−1
+                                 // (bounds the X_hi rounds waiting in L2 for their re-read); 0: unbounded
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
   uint64_t* sfull = sempty + 1;                   // S chain of an own tile complete
   uint64_t* zfull = sfull + 1;                    // all product-2 MMAs complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zfull + 1);
+  volatile int* bdone = reinterpret_cast<volatile int*>(tmem_slot + 1);   // rounds the B-stream has loaded
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x % p.ndg, r = blockIdx.x / p.ndg;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
     mbar_init(sempty, 4);
     mbar_init(sfull, 1);
     mbar_init(zfull, 1);
+    *bdone = 0;
     fence_barrier_init();
   }
   if (warp == W_XPROD && lane == 0) {
@@ -156,6 +160,8 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
       for (int64_t rho = 0; rho < nrounds; ++rho) {
         const int64_t t = own_tile(rho);
         if (t < 0) continue;
+        if (p.lag > 0)
+          while (*bdone < rho - p.lag) __nanosleep(64);
         for (int64_t kc = 0; kc < p.nk; ++kc, ++it) {
           const uint32_t s = it % NSTA, ph = (it / NSTA) & 1;
           if (p.pf) prefetch();
@@ -200,6 +206,7 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
         const uint32_t s = q % NSTB, ph = (q / NSTB) & 1;
         mbar_wait(&bfull[s], ph);
         tc_fence_after();
+        if ((q + 1) % ((int64_t)(BM / KR) * p.ndg) == 0) *bdone = (int)((q + 1) / ((BM / KR) * p.ndg));
         const uint32_t xb = smem_u32(sB + s * (BX + BY)), yb = xb + BX;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
