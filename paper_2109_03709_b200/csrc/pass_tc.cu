@@ -163,6 +163,30 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
 // Z[j][x] = Σ_g Zp[g][x][j], g in order (fixed, deterministic).  Block = ZP_XB columns × all mp features:
 // the block's slice of each partial is ZP_XB·mp contiguous floats, read coalesced, with the partials of
 // 8 row groups in flight per thread; the sums leave through shared memory as ZP_XB-float runs of Z's rows.
+// (for many row groups — the fused power pass, nrg ≈ 36 — the per-column kernel below is faster: its
+// 8 warps split the partials; this one serves the short windows of the minibatch steps, nrg ≤ 16)
+// Z[j][x] = Σ_g Zp[g][x][j]: block (x, 32 consecutive j), warp w sums g ≡ w (mod 8) (8 loads in flight),
+// the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
+                                                             int mp, int m, int64_t d, float* __restrict__ Z) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t x = blockIdx.x;
+  const int j = blockIdx.y * 32 + lane;
+  double s = 0.0;
+  if (j < m)
+    s = sum_in_order<8>(warp, nrg, 8, [&](int64_t g) { return (double)Zp[(g * dpad + x) * mp + j]; });
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && j < m) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    Z[(int64_t)j * d + x] = (float)t;
+  }
+}
+
+static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z);
+
 constexpr int ZP_XB = 8;
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z) {
@@ -196,6 +220,13 @@ __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict_
     const int j = e / ZP_XB, xl = e % ZP_XB;
     if (x0 + xl < d) Z[(int64_t)j * d + x0 + xl] = tr[j][xl];
   }
+}
+
+static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z) {
+  if (nrg > 16)
+    reduce_zp_cols_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+  else
+    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
 }
 
 // ============================================================================ host side
@@ -508,7 +539,7 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   kernel_timer_mark(c, 0);
   reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
-  reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+  launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
 }
@@ -586,7 +617,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   else
     PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   kernel_timer_mark(c, 1);
-  reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, bp.nrg, dpad, mp, m, d, Z);
+  launch_reduce_zp(c, Zp, bp.nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
 }
