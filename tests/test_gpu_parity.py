@@ -215,6 +215,30 @@ def test_oja_parity_c2s(P, ctx, split, impl):
     U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, _tol(s), "C2s", th_all_ref)
 
 
+@pytest.mark.parametrize("k,batch,d,dtype,split", [
+    (10, 100, 200, "f32", False),     # m = 20: components not a multiple of 8, ragged windows (n % b = 7)
+    (24, 256, 136, "f32", True),      # m = 48 > 32: two lanes' worth of components per row; split planes
+    (16, 64, 784, "bf16", False),     # bf16 storage, many short windows
+], ids=["m20-b100-f32", "m48-b256-split", "m32-b64-bf16"])
+def test_oja_persistent_shapes(P, ctx, k, batch, d, dtype, split):
+    """The persistent single-kernel Oja (auto pass selection, one GPU) on shapes the configs do not
+    exercise, against the fp64 oracle's trajectory (same seeded data, init and schedule)."""
+    import dataclasses
+    import torch
+    base = C.SMALL["C2s"]
+    spec = dataclasses.replace(base.spec, n=4007, d=d, dtype=dtype)
+    w = dataclasses.replace(base, k=k, l=k, batch=batch, spec=spec, steps=90)
+    Xs, X64 = _host(w)
+    W_ref, _ = O.prime_oja(X64, G.init_gaussians(w.init_seed, w.m, d), w.batch, w.alpha, w.momentum, w.steps)
+    Xm = _device_matrix(P, ctx, Xs, spec, split)
+    W = torch.zeros((w.m, d), dtype=torch.float32, device="cuda")
+    vel = torch.zeros_like(W)
+    assert P.ppca_prime_oja(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, w.steps, w.init_seed, W, vel, 0) == w.steps
+    rel = np.linalg.norm(W.cpu().numpy().astype(np.float64) - W_ref) / np.linalg.norm(W_ref)
+    print(f"\n[parity] oja persistent m={w.m} b={batch} d={d} {dtype}{' split' if split else ''}: drift {rel:.2e}")
+    assert rel < 1e-3
+
+
 def test_oja_persistent_resume_bit_exact(P, ctx):
     """The persistent Oja kernel is deterministic and resumable: 200 steps in one call equal 77 + 123 steps
     through step_io (same W and velocity bits), and the step counter wraps over the epoch boundary."""
