@@ -400,21 +400,79 @@ ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, con
   return run_ka(c, X, Wb, m, mp, S, nullptr, 0, 1, nullptr, plan->tiles_dev, plan->ntiles_sel);
 }
 
-// Y of a K-split row window: Y = Σ_parts Ypart (fixed order) → Yᵀ bf16 pair [2·mp][ldyt] (rows ≥ n zero)
-// and the compact fp32 Y [n][m] for S = YᵀY.
-__global__ void ysum_kernel(const float* __restrict__ Ypart, int ksplit, int64_t n, int mp, int m,
-                            __nv_bfloat16* __restrict__ YT, int64_t ldyt, float* __restrict__ Yc) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)mp * ldyt) return;
-  const int j = (int)(e / ldyt);
-  const int64_t r = e % ldyt;
-  float y = 0.f;
-  if (r < n)
-    for (int q = 0; q < ksplit; ++q) y += Ypart[((int64_t)q * n + r) * mp + j];
-  const __nv_bfloat16 hi = __float2bfloat16_rn(y);
-  YT[(int64_t)j * ldyt + r] = hi;
-  YT[(int64_t)(mp + j) * ldyt + r] = __float2bfloat16_rn(y - __bfloat162float(hi));
-  if (r < n && j < m) Yc[r * m + j] = y;
+// Y of a K-split row window and S = YᵀY in one pass over the partials: block = YS_RB rows.  Y = Σ_parts Ypart
+// in part order (fp32), written as the Yᵀ bf16 pair [Y_hi; Y_lo] [2·mp][ldyt] (rows ≥ n zero) for kernel B;
+// the block's rows also give a partial S_b = Σ_rows y yᵀ (fp64 products and sums, 4×4 register tiles per
+// thread) that launch_reduce_splits_f64 sums in block order.
+constexpr int YS_RB = 32;
+__global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Ypart, int ksplit, int64_t n, int mp,
+                                                     int m, __nv_bfloat16* __restrict__ YT, int64_t ldyt,
+                                                     double* __restrict__ Spart) {
+  extern __shared__ float ysm[];                      // YS_RB × (mp + 1)
+  const int ld = mp + 1;
+  const int64_t r0 = (int64_t)blockIdx.x * YS_RB;
+  const int cnt = YS_RB * mp;
+  for (int e0 = threadIdx.x; e0 < cnt; e0 += 4 * 256) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < ksplit; ++q) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * 256;
+        const int64_t r = r0 + e / mp;
+        v[u] = (e < cnt && r < n) ? Ypart[((int64_t)q * n + r) * mp + e % mp] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * 256;
+      if (e < cnt) ysm[(e / mp) * ld + e % mp] = acc[u];
+    }
+  }
+  __syncthreads();
+  // the Yᵀ pair (rows < ldyt; rows ≥ n are zero)
+  for (int e = threadIdx.x; e < mp * YS_RB; e += 256) {
+    const int j = e / YS_RB, rr = e % YS_RB;
+    if (r0 + rr < ldyt) {
+      const float y = ysm[rr * ld + j];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(y);
+      YT[(int64_t)j * ldyt + r0 + rr] = hi;
+      YT[(int64_t)(mp + j) * ldyt + r0 + rr] = __float2bfloat16_rn(y - __bfloat162float(hi));
+    }
+  }
+  // partial S of the block's rows
+  const int nt4 = mp / 4;
+  double* Sb = Spart + (int64_t)blockIdx.x * m * m;
+  for (int tile = threadIdx.x; tile < nt4 * nt4; tile += 256) {
+    const int bi = tile / nt4, bj = tile % nt4;
+    double a[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) a[u][v] = 0.0;
+    for (int rr = 0; rr < YS_RB; ++rr) {
+      const float* row = ysm + rr * ld;
+      double yi[4], yj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        yi[u] = (double)row[bi * 4 + u];
+        yj[u] = (double)row[bj * 4 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[u][v] = fma(yi[u], yj[v], a[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = bi * 4 + u, j = bj * 4 + v;
+        if (i < m && j < m) Sb[i * m + j] = a[u][v];
+      }
+  }
 }
 
 // K split for short row windows (a minibatch step): enough (tile, K part) items to cover the SMs
@@ -567,12 +625,15 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
     PPCA_TRY(run_ka(c, X, Wb, m, mp, S, YT, ldyt));
   } else {
     float* Ypart = (float*)scratch(c, S_TC3, (size_t)ksplit * n * mp * sizeof(float));
-    float* Yc = (float*)scratch(c, S_TC4, (size_t)n * m * sizeof(float));
-    if (!Ypart || !Yc) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    if (!Ypart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
     PPCA_TRY(run_ka(c, X, Wb, m, mp, S, nullptr, 0, ksplit, Ypart));
-    ysum_kernel<<<(unsigned)ceil_div((int64_t)mp * ldyt, 256), 256, 0, c->stream>>>(Ypart, ksplit, n, mp, m, YT, ldyt, Yc);
-    PPCA_LAUNCH_CHECK(c, "ysum");
-    PPCA_TRY(yty(c, Yc, m, n, S));
+    const int64_t nb = ceil_div(ldyt, (int64_t)YS_RB);
+    double* Sp = (double*)scratch(c, S_NTSTAGE, (size_t)nb * m * m * sizeof(double));
+    if (!Sp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    ysum_s_kernel<<<(unsigned)nb, 256, (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream>>>(Ypart, ksplit, n, mp, m,
+                                                                                              YT, ldyt, Sp);
+    PPCA_LAUNCH_CHECK(c, "ysum_s");
+    PPCA_TRY(launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S));
   }
   // kernel B
   const int nc = kb::Cfg<64>::NC;
