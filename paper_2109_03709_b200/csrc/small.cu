@@ -680,7 +680,19 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
                     [&](int64_t e, float v) { mvs[e] = v; });
     __syncthreads();
     const int64_t x = x0 + lane;
-    for (int j = warp; j < m; j += nw) {
+    // this warp's V and velocity entries, all in flight before the row loop (≤ PPCA_MAX_M / 8 rows per warp)
+    float vpre[PPCA_MAX_M / 8], velpre[PPCA_MAX_M / 8];
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+      const int j = warp + q * nw;
+      const bool ok = j < m && x < d;
+      vpre[q] = ok ? V[(int64_t)j * d + x] : 0.f;
+      velpre[q] = ok ? vel[(int64_t)j * d + x] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+      const int j = warp + q * nw;
+      if (j >= m) break;
       const double* cj = Cf + j * m;
       double t0 = 0.0, t1 = 0.0;
       int i = 0;
@@ -693,9 +705,9 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
       double sq = 0.0;
       if (x < d) {
         const int64_t e = (int64_t)j * d + x;
-        const double r = 2.0 * (double)mvs[j * EG_XC + lane] - 2.0 * (double)tf - twoU[j] * (double)V[e];
-        const double v = mu * (double)vel[e] + r;
-        const double w = (double)V[e] + alpha * (r + mu * v);
+        const double r = 2.0 * (double)mvs[j * EG_XC + lane] - 2.0 * (double)tf - twoU[j] * (double)vpre[q];
+        const double v = mu * (double)velpre[q] + r;
+        const double w = (double)vpre[q] + alpha * (r + mu * v);
         if (!isfinite(w)) atomicOr(d_err, DEV_NONFINITE);
         vel[e] = (float)v;
         const float wf = (float)w;
@@ -708,26 +720,24 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
     __syncthreads();
   }
   grid.sync();
-  // row norms: Σ over chunks in chunk order (every CTA the same sums), then rescale this CTA's columns
-  for (int j = warp; j < m; j += nw) {
-    double s2 = 0.0;
-    for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
-      const int64_t c1 = c0 + lane;
-      double v = c1 < nchunks ? rowpart[c1 * m + j] : 0.0;
-      // fixed-order combination inside the warp (lane order), then across the 32-chunk blocks in order
-      for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_down_sync(0xffffffffu, v, o);
-        if ((lane & (2 * o - 1)) == 0) v += u;
-      }
-      s2 += __shfl_sync(0xffffffffu, v, 0);
-    }
-    const double n = sqrt(s2);
-    if (lane == 0) {
+  // row norms: thread (row j, slice s) sums chunks c ≡ s (mod ns) in order (8 loads in flight), the slices
+  // are added in slice order — the same sums in every CTA; then this CTA's columns are rescaled
+  {
+    const int ns = (int)blockDim.x / m;                   // ≥ 2 for m ≤ 128
+    const int j = threadIdx.x % m, sl = threadIdx.x / m;
+    double* part = reinterpret_cast<double*>(mvs);        // ns × m (the MV slab is free now)
+    if (sl < ns)
+      part[sl * m + j] = sum_in_order<8>(sl, nchunks, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
+    __syncthreads();
+    if (threadIdx.x < m) {
+      double s2 = 0.0;
+      for (int q = 0; q < ns; ++q) s2 += part[q * m + threadIdx.x];
+      const double n = sqrt(s2);
       if (!(n > 1e-300)) {
         if (blockIdx.x == 0) atomicOr(d_err, DEV_DEGENERATE);
-        nrm[j] = 0.0;
+        nrm[threadIdx.x] = 0.0;
       } else {
-        nrm[j] = 1.0 / n;
+        nrm[threadIdx.x] = 1.0 / n;
       }
     }
   }
@@ -750,7 +760,8 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
                                    double alpha, double mu, ppca_status* st) {
   *st = PPCA_OK;
   const int64_t nchunks = ceil_div(d, (int64_t)EG_XC);
-  const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) + (size_t)m * EG_XC * sizeof(float);
+  const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) +
+                      std::max((size_t)m * EG_XC * sizeof(float), (size_t)256 * sizeof(double));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(eg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
