@@ -160,14 +160,24 @@ __device__ void oja_steps(const OjaParams& p, const T* __restrict__ X, uint8_t* 
           __syncthreads();
           if (p.xvec) {
             const int per = (int)(d / 8), cnt = rg * per;
-            for (int e = tid; e < cnt; e += OJA_THREADS) {
-              const int rr = e / per, x8 = (e - rr * per) * 8;
-              double o[8];
-              load_row8(X, p, r0 + rr0 + (rr < nr ? rr : nr - 1), x8, o);
-              float4* dst = reinterpret_cast<float4*>(Xr + (size_t)rr * d + x8);
-              const float z = rr < nr ? 1.f : 0.f;
-              dst[0] = make_float4(z * (float)o[0], z * (float)o[1], z * (float)o[2], z * (float)o[3]);
-              dst[1] = make_float4(z * (float)o[4], z * (float)o[5], z * (float)o[6], z * (float)o[7]);
+            for (int e0 = tid; e0 < cnt; e0 += 4 * OJA_THREADS) {   // four 8-element groups in flight
+              double o[4][8];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int e = min(e0 + u * OJA_THREADS, cnt - 1);
+                const int rr = e / per, x8 = (e - rr * per) * 8;
+                load_row8(X, p, r0 + rr0 + (rr < nr ? rr : nr - 1), x8, o[u]);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * OJA_THREADS;
+                if (e >= cnt) break;
+                const int rr = e / per, x8 = (e - rr * per) * 8;
+                float4* dst = reinterpret_cast<float4*>(Xr + (size_t)rr * d + x8);
+                const float z = rr < nr ? 1.f : 0.f;
+                dst[0] = make_float4(z * (float)o[u][0], z * (float)o[u][1], z * (float)o[u][2], z * (float)o[u][3]);
+                dst[1] = make_float4(z * (float)o[u][4], z * (float)o[u][5], z * (float)o[u][6], z * (float)o[u][7]);
+              }
             }
           } else {
             stage16(Xr, (int)(rg * d), [&](int e) {
