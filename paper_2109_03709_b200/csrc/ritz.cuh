@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
         }
       }
       if (fabs(d[m - 1]) < tiny) d[m - 1] = d[m - 1] < 0.0 ? -tiny : tiny;
+      // U's diagonal as reciprocals once (the solves below then multiply: 3·m fp64 divisions saved)
+      for (int i = 0; i < m; ++i) d[i] = 1.0 / (fabs(d[i]) < tiny ? (d[i] < 0.0 ? -tiny : tiny) : d[i]);
       for (int i = 0; i < m; ++i) x[i] = 1.0 + 0.37 * sin(0.9 * (double)(i + 1) * (double)(j + 1));
       for (int it = 0; it < 3; ++it) {
         for (int i = 0; i + 1 < m; ++i) {              // L
@@ -409,10 +411,9 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
             x[i + 1] = t - dl[i] * x[i];
           }
         }
-        x[m - 1] /= d[m - 1];                          // U
-        if (m >= 2) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) / (fabs(d[m - 2]) < tiny ? tiny : d[m - 2]);
-        for (int i = m - 3; i >= 0; --i)
-          x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / (fabs(d[i]) < tiny ? tiny : d[i]);
+        x[m - 1] *= d[m - 1];                          // U (d holds 1/U_ii)
+        if (m >= 2) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) * d[m - 2];
+        for (int i = m - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) * d[i];
         for (int jp = j0; jp < j; ++jp) {              // Gram–Schmidt against the cluster's earlier vectors
           double dt = 0.0;
           for (int i = 0; i < m; ++i) dt += XT[i * m + jp] * x[i];
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
         }
         double nn = 0.0;
         for (int i = 0; i < m; ++i) nn += x[i] * x[i];
-        const double rn = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        const double rn = nn > 0.0 ? rsqrt(nn) : 0.0;
         for (int i = 0; i < m; ++i) x[i] *= rn;
       }
       for (int i = 0; i < m; ++i) XT[i * m + j] = x[i];
