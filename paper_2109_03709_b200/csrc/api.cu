@@ -77,6 +77,9 @@ void* scratch(Ctx* c, int slot, size_t bytes) {
     c->slot_bytes[slot] = 0;
   }
   size_t want = bytes + bytes / 4;
+  static int dbg = -1;
+  if (dbg < 0) dbg = getenv("PPCA_DEBUG_SCRATCH") ? 1 : 0;
+  if (dbg) fprintf(stderr, "[ppca] scratch slot %d grows to %zu bytes\n", slot, want);
   void* p = nullptr;
   if (cudaMalloc(&p, want) != cudaSuccess) {
     cudaGetLastError();
