@@ -109,7 +109,8 @@ __device__ void block_cholesky(double* A, int m, double drop, int* keep, double*
       for (int j = kb; j < ke; ++j) {
         const double p = A[j * lda + j];
         const bool dr = drop > 0.0 ? !(p > drop * drop * diag0[j]) : (!(p > 0.0) || !isfinite(p));
-        const double piv = dr ? 0.0 : sqrt(p), rp = dr ? 0.0 : 1.0 / piv;
+        // 1/L_jj by one fp64 rsqrt (62 cycles, vs sqrt + divide ≈ 300 on this serial chain), L_jj = p/√p
+        const double rp = dr ? 0.0 : rsqrt(p), piv = p * rp;
         const int i = j + 1 + lane;
         const double lij = i < ke ? A[i * lda + j] * rp : 0.0;
         __syncwarp();
