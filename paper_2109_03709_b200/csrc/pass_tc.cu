@@ -506,14 +506,13 @@ template <int XM>
 static void launch_fused_cfg(Ctx* c, int cfg, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
                              const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const CUtensorMap& tmY,
                              const KFParams& fp) {
-  // (X stages, W' stages, B stages): the L2-fed B-stream is the limiter, so it gets the deepest ring
-  // (measured on C3: (2,2,5) 0.99 ms, (3,2,4) 1.05, (3,3,3) 1.09, (4,3,2) 1.15); PPCA_FUSED_CFG selects others
+  // (X stages, W' stages, B stages of KR = 64 rows).  Measured on C3, one box: 32-row B stages (2,2,5)
+  // 1.088 ms -> 64-row B stages (2,2,2) 0.951 ms, (3,2,2) 0.993, (2,1,3) 1.018 (larger TMA boxes and half
+  // the B-stream barrier round trips); PPCA_FUSED_CFG selects the others
   switch (cfg) {
-    case 1: launch_fused<XM, 4, 3, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    case 2: launch_fused<XM, 3, 2, 4>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    case 3: launch_fused<XM, 3, 3, 3>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    case 4: launch_fused<XM, 2, 1, 6>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    default: launch_fused<XM, 2, 2, 5>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 6: launch_fused<XM, 3, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 7: launch_fused<XM, 2, 1, 3>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    default: launch_fused<XM, 2, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
   }
 }
 

@@ -12,8 +12,8 @@
 // round ρ in every CTA.  All CTAs are co-resident (persistent, ≤ one per SM), so the flag waits terminate.
 //
 // TMEM (512 columns): Y accumulator [0, 128) (one buffer), S [128, 256), Zᵀ [256, 512) (two 128-row d-chunks
-// × N = 128 = [Y_hi; Y_lo]).  Shared memory: A ring 4 × 32 KB (hi + lo planes), W' ring 3 × 16 KB, B ring
-// 2 × 24 KB (X_hi 32 rows × 256 columns + Y 32 rows × [Y_hi | Y_lo], both MN-major).  S = YᵀY of an own tile
+// × N = 128 = [Y_hi; Y_lo]).  Shared memory (default configuration): A ring 2 × 32 KB (hi + lo planes), W' ring
+// 2 × 16 KB, B ring 2 × 48 KB (X_hi 64 rows × 256 columns + Y 64 rows × [Y_hi | Y_lo], both MN-major).  S = YᵀY of an own tile
 // is chained on the B-stream from the same staged Y rows (no separate Y operand tile).
 // The Y rows go through global memory row-major (one 256-byte store per row) for the siblings.
 // Numerics are those of kernels A2 + B: the same MMAs in the same order per tile.
@@ -23,7 +23,7 @@ namespace kf {
 constexpr int BM = 128, BK = 64, KSEG = 16, SFLUSH = 8;
 constexpr int MP = 64, NB = 2 * MP;            // m padded; product-1 N and product-2 N ([Y_hi; Y_lo])
 constexpr int DG = 256, NC = DG / 128;         // d-group width, 128-row d chunks per group
-constexpr int KR = 32;                         // rows per B stage
+constexpr int KR = 64;                         // rows per B stage (64: 12 % faster than 32 on C3, measured)
 constexpr uint32_t XPL = BM * 128;             // one bf16 plane chunk: 128 rows × 64 columns
 constexpr uint32_t WST = NB * 128;             // W' chunk: 128 rows ([W_hi; W_lo]) × 64 columns
 constexpr uint32_t BBLK = KR * 128;            // KR rows × 64 columns (SW128 atoms of 8 rows)
