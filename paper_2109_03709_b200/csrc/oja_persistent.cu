@@ -503,6 +503,10 @@ bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha
   void* args[] = {&p};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)oja_persistent_kernel, grid, OJA_THREADS, args, OJA_SMEM,
                                               c->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {   // not all CTAs co-resident here (e.g. a shared GPU):
+    cudaGetLastError();                               // the per-step launch sequence runs instead
+    return false;
+  }
   ++c->launches;
   c->last_impl = 1;
   if (e != cudaSuccess) {

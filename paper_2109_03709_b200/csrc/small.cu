@@ -783,6 +783,10 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
   void* args[] = {(void*)&MV, (void*)&A, (void*)&V, (void*)&vel, (void*)&m, (void*)&d, (void*)&alpha, (void*)&mu,
                   (void*)&rowpart, (void*)&c->d_err};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)eg_update_kernel, grid, 256, args, smem, c->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {     // not all CTAs co-resident: the 5-launch sequence runs
+    cudaGetLastError();
+    return false;
+  }
   ++c->launches;
   if (e != cudaSuccess) *st = check_cuda(c, e, "eg_update_kernel");
   return true;
