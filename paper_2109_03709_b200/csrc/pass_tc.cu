@@ -262,13 +262,29 @@ static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap&
   return PPCA_OK;
 }
 
-template <int MP, int XM>
+template <int MP, int XM, bool PAIR = false>
 static ppca_status launch_ka2(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
                               const KAParams& kp, int grid) {
-  const size_t smem = ka2::Cfg<MP, XM>::SMEM;
-  auto kern = xw_tma_kernel<MP, XM>;
+  const size_t smem = ka2::Cfg<MP, XM, PAIR>::SMEM;
+  auto kern = xw_tma_kernel<MP, XM, PAIR>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, ka2::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, kp);
+  if constexpr (!PAIR) {
+    kern<<<grid, ka2::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, kp);
+  } else {                                          // CTA pairs: clusters of 2
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(ka2::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmXlo, kp);
+  }
   PPCA_LAUNCH_CHECK(c, "xw_tma_kernel");
   return PPCA_OK;
 }
@@ -354,8 +370,15 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
 static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, int mp, double* S,
                           __nv_bfloat16* YT, int64_t ldyt, int ksplit = 1, float* Ypart = nullptr,
                           const int32_t* tiles = nullptr, int64_t ntiles_sel = -1) {
+  // kernel A2 on CTA pairs (2-CTA UMMA, W' split across the pair): bf16 X with m padded to 128 (C5), whole
+  // tiles; PPCA_A2_PAIR=0 disables
+  static int pair_env = -1;
+  if (pair_env < 0) pair_env = getenv("PPCA_A2_PAIR") ? atoi(getenv("PPCA_A2_PAIR")) : 1;
+  const bool pair = pair_env && X->dtype == PPCA_BF16 && mp == 128 && ksplit == 1 && tiles == nullptr &&
+                    persistent_ctas(c) >= 2;
   CUtensorMap tmW, tmX, tmXlo;
-  if (!make_map_bf16(&tmW, Wb, X->d, 2 * mp, X->d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
+  if (!make_map_bf16(&tmW, Wb, X->d, 2 * mp, X->d, pair ? mp : 2 * mp))
+    return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
   tmX = tmXlo = tmW;   // unused unless X is staged by TMA
   if (X->dtype != PPCA_F32 && !make_x_maps(X, 128, &tmX, &tmXlo)) return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
   KAParams kp;
@@ -371,6 +394,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
   kp.dbg = dbg;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit));
+  if (pair) grid = (int)std::max<int64_t>(2, std::min<int64_t>(persistent_ctas(c) & ~1, 2 * ((kp.ntiles + 1) / 2)));
   // TMA-staged X (bf16, split) runs kernel A2; its S partial has 2·mp rows when S is on the tensor cores
   const bool tma_x = X->dtype != PPCA_F32;
   const bool smma = tma_x && mp == 64;
@@ -378,7 +402,8 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   if (!Spart) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   kp.Spart = Spart;
   kernel_timer_mark(c, 0);
-  PPCA_TRY(X->dtype == PPCA_BF16        ? dispatch_ka2<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
+  PPCA_TRY(pair                          ? (launch_ka2<128, 1, true>(c, tmW, tmX, tmXlo, kp, grid))
+           : X->dtype == PPCA_BF16        ? dispatch_ka2<1>(c, mp, tmW, tmX, tmXlo, kp, grid)
            : X->dtype == PPCA_F32_SPLIT ? dispatch_ka2<2>(c, mp, tmW, tmX, tmXlo, kp, grid)
                                         : dispatch_ka<0>(c, mp, tmW, tmX, tmXlo, kp, grid));
   kernel_timer_mark(c, 0);

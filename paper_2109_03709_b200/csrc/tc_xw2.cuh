@@ -31,7 +31,7 @@ constexpr uint32_t XST = BM * 128; // one bf16 plane stage (128 rows × 64 colum
 constexpr uint32_t YBLK = BM * 128;   // one 64-feature block of the Y operand tile
 constexpr int XPF = 0;             // X chunks prefetched into L2 ahead of the TMA loads (measured: hurts)
 
-template <int MP, int XM>
+template <int MP, int XM, bool PAIR = false>
 struct Cfg {
   static constexpr bool SMMA = MP == 64;                        // S on the tensor cores
   static constexpr int NB = 2 * MP;                             // product-1 UMMA N: [W_hi; W_lo]
@@ -44,8 +44,9 @@ struct Cfg {
   static constexpr uint32_t XSTG = PLANES * XST;
   // W' stages: a 2·MP-row W' chunk is as large as (MP = 64) or twice (MP = 128) the X chunk it multiplies and
   // comes from L2, so its ring must cover L2 latency too (measured on C5: 2 stages starve the MMA)
-  static constexpr int NWS = MP <= 64 ? 4 : (XM == 1 ? 3 : 2);
-  static constexpr uint32_t WST = NB * 128;
+  // PAIR (2-CTA UMMA, M = 256): each CTA of the pair holds half of every W' chunk (NB/2 rows)
+  static constexpr int NWS = PAIR ? 4 : (MP <= 64 ? 4 : (XM == 1 ? 3 : 2));
+  static constexpr uint32_t WST = (PAIR ? NB / 2 : NB) * 128;
   // fp32 Y rows for the CUDA-core S (the tensor-core S keeps the segment sums in registers)
   static constexpr size_t YS = SMMA ? 0 : (size_t)BM * (MP + 4) * 4;
   static constexpr size_t YSM = SMMA ? (size_t)2 * YBLK : 0;    // bf16 [Y_hi | Y_lo] operand tile
@@ -57,12 +58,17 @@ struct Cfg {
 };
 }  // namespace ka2
 
-template <int MP, int XM>
+// PAIR: CTA pairs (cluster of 2) share one 2-CTA UMMA (M = 256 rows: tile 2q+r in CTA r; W' split by N across
+// the pair, so each CTA streams half of every W' chunk from L2).  Rank 1's TMA loads complete on rank 0's
+// stage barriers (.cta_group::2), rank 0 issues the MMAs, completions are multicast to both CTAs' barriers;
+// each CTA drains its own TMEM rows (rank 1's epilogue releases rank 0's TMEM-empty barrier remotely).  Used for MP = 128 with bf16 X (C5), whole tiles, no tile list.
+template <int MP, int XM, bool PAIR = false>
 __global__ void __launch_bounds__(ka2::NTHREADS, 1)
     xw_tma_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, KAParams p) {
   using namespace ka2;
-  using CF = Cfg<MP, XM>;
+  using CF = Cfg<MP, XM, PAIR>;
+  static_assert(!PAIR || (MP == 128 && XM == 1), "kernel A2 pairs: MP = 128, bf16 X");
   constexpr int NST = CF::NST, NWS = CF::NWS, NTB = CF::NTB, NB = CF::NB;
   constexpr uint32_t XSTG = CF::XSTG, WST = CF::WST, TCOLS = CF::TCOLS;
   constexpr bool SMMA = CF::SMMA, LO = XM == 2;
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
     }
     for (int b = 0; b < NTB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], PAIR ? 8 : 4);
     }
     mbar_init(yfull, 4);
     mbar_init(sfull, 1);
@@ -109,15 +115,29 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
     tma_prefetch_desc(&tmX);
     if (LO) tma_prefetch_desc(&tmXlo);
   }
-  if (warp == W_MMA) tmem_alloc<TCOLS>(tmem_slot);
+  if (warp == W_MMA) {
+    if constexpr (PAIR) tmem_alloc_pair<TCOLS>(tmem_slot);
+    else tmem_alloc<TCOLS>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_barrier();            // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // work item = (row tile, K part): t = it / ksplit, chunks [k0, k1) (ksplit = 1: whole tiles)
-  const int64_t nitems = p.ntiles * p.ksplit, i0 = blockIdx.x, istep = gridDim.x;
+  const uint32_t rank = PAIR ? pair_rank() : 0;
+  // work item = (row tile, K part): t = it / ksplit, chunks [k0, k1) (ksplit = 1: whole tiles); PAIR: item =
+  // tile pair q, this CTA's tile 2q + rank
+  const int64_t nitems = PAIR ? (p.ntiles + 1) / 2 : p.ntiles * p.ksplit;
+  const int64_t i0 = PAIR ? blockIdx.x / 2 : blockIdx.x, istep = PAIR ? gridDim.x / 2 : gridDim.x;
   const bool partial = p.ksplit > 1;
   auto item = [&](int64_t it, int64_t& t, int64_t& k0, int64_t& k1, int64_t& nseg) {
+    if constexpr (PAIR) {
+      t = 2 * it + rank;
+      k0 = 0;
+      k1 = p.nk;
+      nseg = (k1 - k0 + KSEG - 1) / KSEG;
+      return;
+    }
     t = p.tiles ? (int64_t)p.tiles[it / p.ksplit] : it / p.ksplit;
     k0 = (it % p.ksplit) * p.kper;
     k1 = min(p.nk, k0 + p.kper);
@@ -134,8 +154,13 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         for (int64_t kc = k0; kc < k1; ++kc, ++it) {
           const uint32_t s = it % NWS, ph = (it / NWS) & 1;
           mbar_wait(&wempty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&wfull[s], WST);
-          tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
+          if (PAIR && rank == 1) {                    // rank 1's half signals rank 0's barrier
+            tma_load_2d_to_peer_bar(sW + s * WST, &tmW, &wfull[s], 0, (int32_t)(kc * BK), (int32_t)(NB / 2),
+                                    policy_evict_last());
+          } else {
+            mbar_arrive_expect_tx(&wfull[s], PAIR ? 2 * WST : WST);
+            tma_load_2d(sW + s * WST, &tmW, &wfull[s], (int32_t)(kc * BK), 0);
+          }
         }
       }
     } else if (warp == W_XPROD && lane == 0) {
@@ -148,15 +173,21 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         for (int64_t kc = k0; kc < k1; ++kc, ++it) {
           const uint32_t s = it % NST, ph = (it / NST) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], (p.dbg & 64) ? XST : XSTG);
+          if (PAIR && rank == 1) {
+            tma_load_2d_to_peer_bar(sX + s * XSTG, &tmX, &full[s], 0, (int32_t)(kc * BK), (int32_t)(t * BM), pol);
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[s], PAIR ? 2 * XSTG : ((p.dbg & 64) ? XST : XSTG));
           tma_load_2d_hint(sX + s * XSTG, &tmX, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
           if (LO && !(p.dbg & 64))
             tma_load_2d_hint(sX + s * XSTG + XST, &tmXlo, &full[s], (int32_t)(kc * BK), (int32_t)(t * BM), pol);
         }
       }
+    } else if (PAIR && warp == W_MMA && rank == 1) {
+      // pair rank 1 issues no MMAs: its stages signal rank 0's barriers directly (TMA .cta_group::2)
     } else if (warp == W_MMA && lane == 0) {
       // ---------------------------------------------------------------- MMA issue (one thread)
-      constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, BM, NB, 0, 0);
+      constexpr uint32_t ID = idesc(FMT_BF16, FMT_BF16, PAIR ? 2 * BM : BM, NB, 0, 0);
       constexpr uint32_t ID_HI = idesc(FMT_BF16, FMT_BF16, BM, MP, 0, 0);
       constexpr uint32_t ID_S = idesc(FMT_BF16, FMT_BF16, 128, 128, 1, 1);   // Y tile MN-major
       auto issue_s = [&](uint32_t j) {
@@ -176,7 +207,8 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
         item(mi, t, k0, k1, nseg);
         for (int64_t g = 0; g < nseg; ++g, ++sg) {
           const uint32_t b = sg % NTB, tph = (sg / NTB) & 1;
-          mbar_wait(&tempty[b], tph ^ 1);
+          if constexpr (PAIR) mbar_wait_cluster(&tempty[b], tph ^ 1);
+          else mbar_wait(&tempty[b], tph ^ 1);
           tc_fence_after();
           const uint32_t dcol = tmem + b * NB;
           const int64_t g0 = k0 + g * KSEG, g1 = min(k1, g0 + KSEG);
@@ -189,16 +221,27 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
             const uint32_t xa = smem_u32(sX + s * XSTG), wa = smem_u32(sW + ws * WST);
 #pragma unroll
             for (int kk = 0; kk < BK / 16 && !(p.dbg & 1); ++kk) {
-              mma_bf16(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024), ID,
-                       (kc != g0) || kk != 0);
-              if (LO)
-                mma_bf16(dcol, smem_desc_sw128(xa + XST + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024),
-                         ID_HI, 1);
+              if constexpr (PAIR) {
+                mma_bf16_pair(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024),
+                              ID, (kc != g0) || kk != 0);
+              } else {
+                mma_bf16(dcol, smem_desc_sw128(xa + kk * 32, 16, 1024), smem_desc_sw128(wa + kk * 32, 16, 1024), ID,
+                         (kc != g0) || kk != 0);
+                if (LO)
+                  mma_bf16(dcol, smem_desc_sw128(xa + XST + kk * 32, 16, 1024),
+                           smem_desc_sw128(wa + kk * 32, 16, 1024), ID_HI, 1);
+              }
             }
-            mma_commit(&empty[s]);
-            mma_commit(&wempty[ws]);
+            if constexpr (PAIR) {
+              mma_commit_pair(&empty[s], 3);
+              mma_commit_pair(&wempty[ws], 3);
+            } else {
+              mma_commit(&empty[s]);
+              mma_commit(&wempty[ws]);
+            }
           }
-          mma_commit(&tfull[b]);
+          if constexpr (PAIR) mma_commit_pair(&tfull[b], 3);
+          else mma_commit(&tfull[b]);
         }
         // S of the previous tile, issued behind this tile's product 1 so the tensor pipe never waits
         // for the epilogue
@@ -263,7 +306,10 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[b]);
+          if (lane == 0) {
+            if (PAIR && rank == 1) mbar_arrive_peer(&tempty[b], 0);
+            else mbar_arrive(&tempty[b]);
+          }
         }
         const int64_t grow = t * BM + tid;
         if (partial) {                                   // K part of a row window: fp32 partial Y out
@@ -342,7 +388,10 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[b]);
+          if (lane == 0) {
+            if (PAIR && rank == 1) mbar_arrive_peer(&tempty[b], 0);
+            else mbar_arrive(&tempty[b]);
+          }
         }
         const int64_t grow = t * BM + tid;
         if (partial) {
@@ -389,5 +438,10 @@ __global__ void __launch_bounds__(ka2::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == W_MMA) tmem_dealloc<TCOLS>(tmem);
+  if constexpr (PAIR) {
+    cluster_barrier();                                // no remote arrive may target an exited CTA
+    if (warp == W_MMA) tmem_dealloc_pair<TCOLS>(tmem);
+  } else {
+    if (warp == W_MMA) tmem_dealloc<TCOLS>(tmem);
+  }
 }
