@@ -449,26 +449,44 @@ def run_minibatch(args, w, rank, world, local_rank):
         per_epoch = -(-s.n // w.batch)
         checkpoints = sorted(set([2 ** j for j in range(4, 13)] + [per_epoch * e for e in range(1, 31)]))
         cap = 30 * per_epoch if w.priming == "oja" else 4096       # reading R21
-        step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, 0, w.init_seed, V2, vel2, 0)
-        P.ppca_refine(ctx, Xm, V2, w.m, w.k, E)      # untimed warm-up: the refine's scratch and kernels
-        torch.cuda.synchronize()
-        reached, t_ms = None, 0.0
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for cp in checkpoints:
-            if cp > cap:
-                break
-            e0.record(stream)
-            step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, cp - step, 0, V2, vel2, step)
-            P.ppca_refine(ctx, Xm, V2, w.m, w.k, E)                  # charged refine (S L429)
-            e1.record(stream)
+        def ttl_run(fraction):
+            """priming from the seeded start, a charged refine at every checkpoint until LCES = k; fraction < 1:
+            the refine projects a seeded 10 % row-tile sample (P L378, reading R25)"""
+            def refine():
+                if fraction >= 1.0:
+                    P.ppca_refine(ctx, Xm, V2, w.m, w.k, E)
+                else:
+                    P.ppca_refine_sampled(ctx, Xm, V2, w.m, w.k, E, fraction, 4242)
+            vel2.zero_()
+            step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, 0, w.init_seed, V2, vel2, 0)
+            refine()                                     # untimed warm-up: the refine's scratch and kernels
             torch.cuda.synchronize()
-            t_ms += e0.elapsed_time(e1)
-            _, lc = P.ppca_eval(ctx, E, Tt, w.k, s.d, [thr])
-            if lc[0] >= w.k:
-                reached = cp
-                break
+            step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, 0, w.init_seed, V2, vel2, 0)
+            reached, t_ms = None, 0.0
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for cp in checkpoints:
+                if cp > cap:
+                    break
+                e0.record(stream)
+                step = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, cp - step, 0, V2, vel2, step)
+                refine()                                 # charged refine (S L429)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t_ms += e0.elapsed_time(e1)
+                _, lc = P.ppca_eval(ctx, E, Tt, w.k, s.d, [thr])
+                if lc[0] >= w.k:
+                    reached = cp
+                    break
+            return reached, t_ms
+
+        reached, t_ms = ttl_run(1.0)
         ttl = {"target": f"LCES={w.k} at V={thr:.6f}", "steps": reached,
-               "ms": t_ms if reached else None, "checkpoints": "2^j and every epoch, refine charged"}
+               "ms": t_ms if reached else None, "checkpoints": "2^j and every epoch, refine charged",
+               "refine": "full projection"}
+        if s.n >= 1_000_000:                             # the paper's large-n setting: project 10 % (P L378)
+            r2, t2 = ttl_run(0.1)
+            ttl["sampled_refine"] = {"steps": r2, "ms": t2 if r2 else None,
+                                     "refine": "seeded 10 % row-tile sample (P L378, reading R25)"}
     P.ppca_ctx_destroy(ctx)
     if rank != 0:
         return 0
