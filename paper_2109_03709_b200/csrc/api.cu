@@ -343,6 +343,13 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   ppca_status st = PPCA_OK;
   c->side_busy = theta_hist_host != nullptr;
   c->prep_ev = theta_hist_host ? ev_prep : nullptr;
+  // one GPU with the θ history: S only feeds the side-stream Ritz solve, so its reduction moves there too
+  c->s_defer = theta_hist_host != nullptr && c->world == 1;
+  if (c->s_defer) {
+    cudaEventCreateWithFlags(&c->s_ev_pass, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->s_ev_red, cudaEventDisableTiming);
+    cudaEventRecord(c->s_ev_red, c->side);
+  }
   for (int t = 0; t < iters && st == PPCA_OK; ++t) {
     double* S = Sbuf + (size_t)(t & 1) * m * m;
     double* Bm = Sbuf + (size_t)(2 + (t & 1)) * m * m;
@@ -356,6 +363,8 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       st = vec_gram_on(c, plan.Wop, m, d, Bm, c->side, S_SIDE_PART);
       if (st != PPCA_OK) break;
       cudaEventRecord(ev_gram, c->side);
+      st = pass_reduce_deferred_s(c, S, c->side);   // after the Gram: that one overlaps the pass
+      if (st != PPCA_OK) break;
     }
     st = allreduce(c, Z, (size_t)m * d, false);
     if (st == PPCA_OK) st = allreduce(c, S, (size_t)m * m, true);
@@ -374,7 +383,14 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   }
   c->prep_ev = nullptr;
   c->side_busy = false;
+  if (c->s_pending) pass_reduce_deferred_s(c, Sbuf, c->side);   // an aborted loop: drain (result unused)
   ppca_status st2 = finish(c, "ppca_prime_power");
+  if (c->s_defer) {
+    cudaEventDestroy(c->s_ev_pass);
+    cudaEventDestroy(c->s_ev_red);
+    c->s_ev_pass = c->s_ev_red = nullptr;
+    c->s_defer = false;
+  }
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(ev_main[i]);
     cudaEventDestroy(ev_side[i]);

@@ -31,6 +31,14 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // side stream (Ritz solves overlap the next pass)
   cudaEvent_t prep_ev = nullptr;     // when set: recorded once the pass operand W' is prepared (power loop)
+  // deferred S reduction of the fused pass (power loop with θ history on one GPU: S feeds only the side-stream
+  // Ritz solve): the pass records s_ev_pass and leaves the partials; pass_reduce_deferred_s reduces them on a
+  // given stream and records s_ev_red, which the next fused pass waits for before rewriting the partials
+  bool s_defer = false;
+  bool s_pending = false;
+  cudaEvent_t s_ev_pass = nullptr, s_ev_red = nullptr;
+  const double* s_part = nullptr;
+  int s_parts = 0, s_mp = 0, s_m = 0;
   bool side_busy = false;             // side-stream kernels may overlap the next pass: persistent
                                       // pass kernels then leave one SM free (a late CTA stalls the pass)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;

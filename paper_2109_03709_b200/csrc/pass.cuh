@@ -34,4 +34,7 @@ ppca_status xw(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const flo
 ppca_status ytx(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const float* Y, int m, float* Z);
 ppca_status yty(Ctx* c, const float* Y, int m, int64_t rows, double* S);
 
+// the fused pass's deferred S reduction (Ctx::s_defer) on stream st; no-op when nothing is pending
+ppca_status pass_reduce_deferred_s(Ctx* c, double* S, cudaStream_t st);
+
 }  // namespace ppca

@@ -610,6 +610,7 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   // −1.6 %; 1 round starves the overlap, 3 = unbounded); PPCA_FUSED_LAG overrides (0 = off)
   if (lag < 0) lag = getenv("PPCA_FUSED_LAG") ? atoi(getenv("PPCA_FUSED_LAG")) : 2;
   fp.lag = lag;
+  if (c->s_defer) cudaStreamWaitEvent(c->stream, c->s_ev_red, 0);   // the previous S partials were reduced
   kernel_timer_mark(c, 0);
   static int cfg = -1;
   if (cfg < 0) cfg = getenv("PPCA_FUSED_CFG") ? atoi(getenv("PPCA_FUSED_CFG")) : 0;
@@ -619,10 +620,30 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
     launch_fused_cfg<1>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
   PPCA_LAUNCH_CHECK(c, "xwz_fused_kernel");
   kernel_timer_mark(c, 0);
-  reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
-  PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  if (c->s_defer) {                               // S is reduced later, on the stream that consumes it
+    cudaEventRecord(c->s_ev_pass, c->stream);
+    c->s_pending = true;
+    c->s_part = Spart;
+    c->s_parts = grid;
+    c->s_mp = mp;
+    c->s_m = m;
+  } else {
+    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  }
   launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
+  return PPCA_OK;
+}
+
+ppca_status pass_reduce_deferred_s(Ctx* c, double* S, cudaStream_t st) {
+  if (!c->s_pending) return PPCA_OK;
+  cudaStreamWaitEvent(st, c->s_ev_pass, 0);
+  reduce_spart2_kernel<<<(unsigned)ceil_div(c->s_m * c->s_m, 32), 256, 0, st>>>(c->s_part, c->s_parts, c->s_mp,
+                                                                               c->s_m, S);
+  PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  cudaEventRecord(c->s_ev_red, st);
+  c->s_pending = false;
   return PPCA_OK;
 }
 
