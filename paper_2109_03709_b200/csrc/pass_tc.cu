@@ -439,16 +439,20 @@ __global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Y
   const int cnt = YS_RB * mp;
   for (int e0 = threadIdx.x; e0 < cnt; e0 += 4 * 256) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int q = 0; q < ksplit; ++q) {
-      float v[4];
+    for (int q0 = 0; q0 < ksplit; q0 += 4) {          // 4 parts × 4 elements = 16 loads in flight
+      float v[4][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * 256;
-        const int64_t r = r0 + e / mp;
-        v[u] = (e < cnt && r < n) ? Ypart[((int64_t)q * n + r) * mp + e % mp] : 0.f;
-      }
+      for (int qq = 0; qq < 4; ++qq)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += v[u];
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * 256;
+          const int64_t r = r0 + e / mp;
+          v[qq][u] = (q0 + qq < ksplit && e < cnt && r < n) ? Ypart[((int64_t)(q0 + qq) * n + r) * mp + e % mp] : 0.f;
+        }
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += v[qq][u];            // part order unchanged
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
