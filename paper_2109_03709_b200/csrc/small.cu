@@ -695,14 +695,20 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
       const int j = warp + q * nw;
       if (j >= m) break;
       const double* cj = Cf + j * m;
-      double t0 = 0.0, t1 = 0.0;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;   // four chains, as the apply kernel; 8 loads in flight
       int i = 0;
-      for (; i + 1 < j; i += 2) {
-        t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
-        t1 = fma(cj[i + 1], (double)mvs[(i + 1) * EG_XC + lane], t1);
+      for (; i + 7 < j; i += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a[u] = cj[i + u];
+          b[u] = (double)mvs[(i + u) * EG_XC + lane];
+        }
+        t0 = fma(a[0], b[0], t0); t1 = fma(a[1], b[1], t1); t2 = fma(a[2], b[2], t2); t3 = fma(a[3], b[3], t3);
+        t0 = fma(a[4], b[4], t0); t1 = fma(a[5], b[5], t1); t2 = fma(a[6], b[6], t2); t3 = fma(a[7], b[7], t3);
       }
-      if (i < j) t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
-      const float tf = (float)(t0 + t1);               // T as the apply kernel stores it (fp32)
+      for (; i < j; ++i) t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
+      const float tf = (float)((t0 + t1) + (t2 + t3));   // T as the apply kernel stores it (fp32)
       double sq = 0.0;
       if (x < d) {
         const int64_t e = (int64_t)j * d + x;
