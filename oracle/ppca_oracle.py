@@ -306,6 +306,48 @@ def ppca_refine_sampled(X: np.ndarray, V: np.ndarray, k: int, fraction: float, s
     return E, theta * (X.shape[0] / rows.size), rows.size
 
 
+class DegenerateProjection(OracleError):
+    """S L343: some π_S(e_i) has norm < 1e-10 (relative to ‖e_i‖)."""
+
+
+def check_prop3(X: np.ndarray, V: np.ndarray, T: np.ndarray, upto: int, tol: float = 1e-8):
+    """Proposition 3 (P L293–302; S L337–345).  S = span V with orthonormal basis
+    B = orth(V); C' = (XBᵀ)ᵀ(XBᵀ) is the projected covariance in B (P L260–269); y_i = B t_i are the
+    coordinates of π_S(e_i) (t_i = the i-th true eigenvector, a row of T).  Condition i (1-based):
+    π_S(e_i) maximises Var on the orthogonal complement (within S) of span(π_S(e_1), …, π_S(e_{i−1}))
+    (P L296–300, reading R22's bullet end), tested as: the top eigenvector u_i of P_i C' P_i, with
+    P_i = I − Q_iQ_iᵀ and Q_i an orthonormal basis of y_1 … y_{i−1}, is within angle `tol` of y_i.
+    Returns (flags, angles): angles[i] = ∠(u_i, y_i) in [0, π/2] for every i ≤ upto; flags[i] is
+    true iff conditions 1 … i all hold (S L343: "stops marking true at the first failure"; reading R28).
+    A library eigensolver (numpy.linalg.eigh) serves as the eigen step."""
+    X = np.asarray(X, dtype=np.float64)
+    T = np.asarray(T, dtype=np.float64)
+    if T.shape[0] < upto:
+        raise OracleError("truth has fewer than `upto` vectors")
+    B = gram_schmidt(V, drop_tol=1e-10, drop=True)
+    C = projected_gram(X, B)                              # C' in basis B
+    m = B.shape[0]
+    flags, angs = [], []
+    chain = True
+    for i in range(upto):
+        y = B @ T[i]                                      # π_S(e_i) in basis B
+        if math.sqrt(y @ y) < 1e-10 * math.sqrt(T[i] @ T[i]):
+            raise DegenerateProjection(f"|pi_S(e_{i + 1})| < 1e-10")
+        Q = gram_schmidt(np.array([B @ T[j] for j in range(i)]).reshape(i, m), drop_tol=1e-10, drop=True)
+        P = np.eye(m) - Q.T @ Q                           # projector onto the complement in S
+        M = P @ C @ P
+        w, U = np.linalg.eigh(M)
+        u = U[:, int(np.argmax(w))]                       # the variance maximiser on the complement
+        yh = y / math.sqrt(y @ y)
+        c = abs(float(u @ yh))
+        s = float(np.linalg.norm(u - (u @ yh) * yh))      # sine, accurate at tiny angles
+        a = math.atan2(s, c)
+        angs.append(a)
+        chain = chain and a <= tol
+        flags.append(chain)
+    return flags, np.array(angs)
+
+
 def ritz_values(S: np.ndarray) -> np.ndarray:
     """Ritz values of an orthonormal-basis Gram S (the pPCA eigenvalue estimates)."""
     return jacobi_eigh(S)[0]

@@ -353,3 +353,91 @@ def test_sampled_refine_reduces_to_refine_and_is_unbiased():
         acc += O.projected_gram(X[r], B) * (3000 / r.size)
     acc /= len(seeds)
     assert np.linalg.norm(acc - S_full) / np.linalg.norm(S_full) < 0.05
+
+
+# ----------------------------------------------------------------------------- Prop. 3 checker (NEXT-4)
+def _diag_data(lam):
+    """rows √λ_j e_j: XᵀX = diag(λ) exactly, the true eigenvectors are the unit vectors"""
+    return np.diag(np.sqrt(np.asarray(lam, dtype=np.float64)))
+
+
+def test_prop3_truth_and_containing_span_hold():
+    """S L341/L346 [TRIVIAL]: primed = truth → π_S(e_i) = e_i, every condition holds; a primed set whose span
+    contains the top-k truth (rotated, plus extra random directions) holds for i ≤ k as well."""
+    X = _random_data(2000, 10, 31)
+    lam, T = O.truth(X)
+    flags, ang = O.check_prop3(X, T[:4], T, 4)
+    assert all(flags) and np.all(ang < 1e-12)
+    rng = np.random.default_rng(32)
+    Q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    V = np.vstack([Q @ T[:3], rng.standard_normal((2, 10))])
+    flags, ang = O.check_prop3(X, V, T, 3)
+    assert all(flags) and np.all(ang < 1e-9)
+
+
+def test_prop3_paper_counterexample():
+    """§4.1 (P L195–223): X = {±3e1, ±2e2, ±e3}, priming (ε, 0, √(1−ε²)), (0, 1, 0), ε = 0.01.  Projected
+    variance along e_1^priming is 2(9ε² + (1−ε²)) < 8 (reading R22), so the top direction of the projected
+    data is e_2 and π_S(e_1) ∝ e_1^priming is orthogonal to it: condition 1 fails at angle π/2
+    (S L346 "flag[1] = false"); the pPCA output is (0, 1, 0) first (P L219–222)."""
+    eps = 0.01
+    X = np.array([[3, 0, 0], [-3, 0, 0], [0, 2, 0], [0, -2, 0], [0, 0, 1], [0, 0, -1]], dtype=np.float64)
+    V = np.array([[eps, 0, math.sqrt(1 - eps ** 2)], [0, 1, 0]])
+    T = np.eye(3)
+    flags, ang = O.check_prop3(X, V, T, 2)
+    assert flags == [False, False]
+    assert ang[0] == pytest.approx(math.pi / 2, abs=1e-12)
+    E, _, _, _ = O.ppca_refine(X, V, 2)
+    np.testing.assert_allclose(np.abs(E[0]), [0, 1, 0], atol=1e-12)
+
+
+@pytest.mark.parametrize("delta2,expect", [(0.7, [True, True, True]), (0.9, [False, False, False])])
+def test_prop3_closed_form_threshold_condition1(delta2, expect):
+    """Closed form: XᵀX = diag(λ), S = span(e1 + δe5, e2, e3).  In the basis {f ∝ e1 + δe5, e2, e3} the
+    projected covariance is diagonal with Var(f) = (λ1 + δ²λ5)/(1 + δ²), and π_S(e1) ∝ f.  Condition 1
+    holds iff Var(f) > λ2 ⟺ δ² < (λ1 − λ2)/(λ2 − λ5) = 0.8 for λ = (10, 6, 4, 2, 1, ½); when it fails,
+    the maximiser is e2 ⊥ f: angle π/2."""
+    lam = [10, 6, 4, 2, 1, 0.5]
+    X = _diag_data(lam)
+    d = math.sqrt(delta2)
+    V = np.array([[1, 0, 0, 0, d, 0], [0, 1, 0, 0, 0, 0], [0, 0, 1, 0, 0, 0]], dtype=np.float64)
+    flags, ang = O.check_prop3(X, V, np.eye(6), 3)
+    assert flags == expect
+    np.testing.assert_allclose(ang, [0, 0, 0] if expect[0] else [math.pi / 2, 0, 0], atol=1e-12)
+
+
+def test_prop3_closed_form_condition2_and_chain():
+    """Closed form, second condition: S = span(e1, e2 + δe5, e3) with δ² = 0.8 > (λ2 − λ3)/(λ3 − λ5) = 2/3:
+    on the complement of π_S(e1) = e1 the maximiser is e3, not π_S(e2) ∝ e2 + δe5 (angle π/2); the third
+    condition holds on its own (angle 0) but the chain is broken, so its flag is false (reading R28)."""
+    X = _diag_data([10, 6, 4, 2, 1, 0.5])
+    d = math.sqrt(0.8)
+    V = np.array([[1, 0, 0, 0, 0, 0], [0, 1, 0, 0, d, 0], [0, 0, 1, 0, 0, 0]], dtype=np.float64)
+    flags, ang = O.check_prop3(X, V, np.eye(6), 3)
+    assert flags == [True, False, False]
+    np.testing.assert_allclose(ang, [0, math.pi / 2, 0], atol=1e-12)
+
+
+def test_prop3_condition1_matches_refine():
+    """Independent path: condition 1's angle is ∠(first pPCA vector, π_S(e1)) — the refine's Jacobi solve
+    lifted to R^d against the projection of the true eigenvector computed here with lstsq."""
+    X = _random_data(1500, 8, 41)
+    lam, T = O.truth(X)
+    rng = np.random.default_rng(42)
+    for trial in range(5):
+        V = T[:3] + 0.05 * rng.standard_normal((3, 8))
+        _, ang = O.check_prop3(X, V, T, 1)
+        E, _, _, _ = O.ppca_refine(X, V, 1)
+        coef = np.linalg.lstsq(V.T, T[0], rcond=None)[0]
+        p = V.T @ coef                                      # π_S(e1)
+        p /= np.linalg.norm(p)
+        a = math.acos(min(1.0, abs(float(E[0] @ p))))
+        assert ang[0] == pytest.approx(a, abs=1e-7)
+
+
+def test_prop3_degenerate_projection():
+    """S L343: π_S(e1) = 0 (S ⊥ e1) raises DegenerateProjection."""
+    X = _diag_data([5, 3, 2, 1])
+    V = np.array([[0, 1.0, 0, 0], [0, 0, 1.0, 0]])
+    with pytest.raises(O.DegenerateProjection):
+        O.check_prop3(X, V, np.eye(4), 2)
