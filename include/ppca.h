@@ -175,6 +175,20 @@ ppca_status ppca_refine_sampled(ppca_ctx* ctx, const ppca_matrix* X, const float
                                 double fraction, uint64_t sample_seed, float* E, double* theta_host,
                                 int* subspace_dim, int64_t* rows_used);
 
+/* Proposition 3 checker (§4.2 Prop. 3: "π_S(e_i) maximises Var on the orthogonal
+ * complement of span(π_S(e_1),…)"; reading R28).
+ * S = span V (orthonormalised as ppca_refine does, same drop rule); t_i = row i of T (the true
+ * eigenvectors).  Condition i: the top eigenvector u_i of the projected covariance restricted to the
+ * complement, within S, of span(π_S(t_1),…,π_S(t_{i−1})) is within angle `tol` of π_S(t_i).
+ * X: as ppca_refine (world > 1: row shards, the projected Gram is all-reduced); V: device [m][d];
+ * T: device [upto][d] fp32, upto ≤ PPCA_MAX_M; angles_host: host double[upto] out, ∠(u_i, π_S(t_i)) in
+ * [0, π/2]; flags_host: host int[upto] out, 1 iff conditions 1 … i all hold (the chain breaks at the
+ * first failure).  Errors: DEGENERATE if ‖π_S(t_i)‖ < 1e-10‖t_i‖, SUBSPACE_COLLAPSE if
+ * dim S < upto, INVALID_ARG for null pointers, upto out of range or tol < 0.  Synchronises the stream.
+ * Accuracy: S is spanned by fp32 rows, so angles below ~1e-6 are not resolved (tol is the caller's). */
+ppca_status ppca_check_prop3(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, const float* T,
+                             int upto, double tol, double* angles_host, int* flags_host);
+
 /* Evaluation (§5.3): angle_i = arccos(min(1,|<E_i,T_i>|)) and
  * LCES(V) = #consecutive i from 1 with angle_i < V (strict), for each threshold.
  * E, T: device [k][d] unit rows.  angles_host: double[k]; lces_host: int[nthr]. */

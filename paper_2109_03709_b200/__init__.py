@@ -30,7 +30,8 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled"]
+           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
+           "ppca_check_prop3"]
 
 
 class PPCAError(RuntimeError):
@@ -93,6 +94,7 @@ def load(path: str = LIB_PATH):
         "ppca_refine_sampled": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, D, ctypes.c_uint64, P, P,
                                     ctypes.POINTER(I), ctypes.POINTER(I64)]),
         "ppca_get_kernel_time": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(I64)]),
+        "ppca_check_prop3": (I, [P, ctypes.POINTER(ppca_matrix), P, I, P, I, D, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -312,6 +314,15 @@ def ppca_refine_sampled(ctx, X: ppca_matrix, V, m: int, k: int, E, fraction: flo
                                            _np_ptr(theta), ctypes.byref(dim), ctypes.byref(used)),
            "ppca_refine_sampled")
     return theta, dim.value, used.value
+
+
+def ppca_check_prop3(ctx, X: ppca_matrix, V, m: int, T, upto: int, tol: float = 1e-8) -> tuple[list, np.ndarray]:
+    """Proposition 3 conditions 1 … upto (P L293–302): (flags, angles); flags[i] = conditions 1 … i hold."""
+    ang = np.zeros(upto, dtype=np.float64)
+    fl = np.zeros(upto, dtype=np.int32)
+    _check(ctx, load().ppca_check_prop3(ctx, ctypes.byref(X), _ptr(V), m, _ptr(T), upto, tol, _np_ptr(ang),
+                                        _np_ptr(fl)), "ppca_check_prop3")
+    return [bool(f) for f in fl], ang
 
 
 def ppca_eval(ctx, E, T, k: int, d: int, thresholds) -> tuple[np.ndarray, np.ndarray]:

@@ -585,6 +585,54 @@ ppca_status ppca_refine_sampled(ppca_ctx* h, const ppca_matrix* X, const float* 
   return refine_impl(&h->c, X, V, m, k, fraction, sample_seed, E, theta_host, subspace_dim, rows_used);
 }
 
+// ---------------------------------------------------------------------------- Prop. 3 checker (NEXT-4)
+// PAPER.md §4.2 Prop. 3 (L293-302), reading R28: B = orth(V) as the refine builds it, S = the
+// projected Gram of the pass, G = the Gram of the stacked [B_op; T] (one vector-Gram launch gives BBᵀ — the
+// metric of the operand rows — and the coordinates B t_i together), then prop3_device.
+ppca_status ppca_check_prop3(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, const float* T, int upto,
+                             double tol, double* angles_host, int* flags_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, m));
+  if (!V || !T || !angles_host || !flags_host || upto < 1 || upto > PPCA_MAX_M || !(tol >= 0.0))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "bad check_prop3 args (upto=%d)", upto);
+  const int64_t d = X->d;
+  float* B = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
+  double* S = (double*)scratch(c, S_S, (size_t)2 * m * m * sizeof(double) + 16);
+  if (!B || !S) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream), "copy V"));
+  PPCA_TRY(normalize_rows(c, B, m, d));
+  int mm = m;
+  PPCA_TRY(cholqr2(c, B, m, d, 1e-6, &mm));               // the refine's orth(V) (reading R14)
+  if (mm < upto) {
+    finish(c, "ppca_check_prop3");
+    return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "span V has dimension %d < upto = %d", mm, upto);
+  }
+  PassPlan plan;
+  PPCA_TRY(pass_prepare(c, X, mm, &plan));
+  PPCA_TRY(pass_gram(c, X, &plan, B, mm, S));
+  PPCA_TRY(allreduce(c, S, (size_t)mm * mm, true));
+  const int g = mm + upto;
+  float* stack = (float*)scratch(c, S_P3F, (size_t)g * d * sizeof(float));
+  double* G = (double*)scratch(c, S_GRAM, (size_t)g * g * sizeof(double));
+  if (!stack || !G) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(stack, plan.Wop, (size_t)mm * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                                         c->stream), "stack B"));
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(stack + (size_t)mm * d, T, (size_t)upto * d * sizeof(float),
+                                         cudaMemcpyDeviceToDevice, c->stream), "stack T"));
+  PPCA_TRY(vec_gram(c, stack, g, d, G));
+  std::vector<double> ratio(upto);
+  PPCA_TRY(prop3_device(c, G, g, S, mm, upto, ratio.data(), angles_host));
+  PPCA_TRY(finish(c, "ppca_check_prop3"));
+  bool chain = true;                                       // flag i: conditions 1 … i all hold (R28)
+  for (int i = 0; i < upto; ++i) {
+    chain = chain && angles_host[i] <= tol;
+    flags_host[i] = chain ? 1 : 0;
+  }
+  return PPCA_OK;
+}
+
 // ---------------------------------------------------------------------------- eval / support
 ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_t d, const double* thr_host, int nthr,
                       double* angles_host, int* lces_host) {

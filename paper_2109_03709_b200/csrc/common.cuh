@@ -83,6 +83,8 @@ enum Slot {
   S_SIDE,                          // side-stream m×m work of the power loop (Linv[2], row maps)
   S_SIDE_PART,                     // side-stream split partials (vector Gram)
   S_NTSTAGE,
+  S_P3,                            // Prop. 3 checker workspace (fp64)
+  S_P3F,                           // Prop. 3 checker stacked vectors [B; T] (fp32)
 };
 
 void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory

@@ -843,4 +843,209 @@ ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, d
   return PPCA_OK;
 }
 
+// ============================================================================ Proposition 3 checker (NEXT-4)
+// PAPER.md §4.2 Prop. 3 (L293-302), reading R28.  Inputs: the stacked Gram
+// G = [B; T][B; T]ᵀ (ld g = mm + upto; B = the operand rows of the pass, T = the true eigenvectors) and the
+// projected Gram S = (XBᵀ)ᵀ(XBᵀ).  With L = chol(BBᵀ) the rows of L⁻¹B are an orthonormal basis of
+// span B, the projected covariance in it is C = L⁻¹SL⁻ᵀ and π_S(t_i) has coordinates y_i = L⁻¹(Bt_i).
+// Kernel 1 (one CTA): C, y_i, ‖y_i‖/‖t_i‖ and the identity (the Ritz solve's metric), all fp64 in global
+// scratch (the m×m work is O(m³) ≈ 2 MFLOP — a diagnostic, not a hot path).
+__global__ void __launch_bounds__(256) prop3_coords_kernel(const double* __restrict__ G, int g,
+                                                           const double* __restrict__ S, int mm, int upto,
+                                                           double* __restrict__ A, double* __restrict__ Linv,
+                                                           double* __restrict__ T1, double* __restrict__ C,
+                                                           double* __restrict__ I, double* __restrict__ Y,
+                                                           double* __restrict__ ratio, double* __restrict__ diag0,
+                                                           int* __restrict__ keep, int* d_err) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < mm * mm; e += nt) {
+    const int a = e / mm, b = e % mm;
+    A[e] = G[(int64_t)a * g + b];
+    I[e] = a == b ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  block_cholesky(A, mm, 0.0, keep, diag0, d_err, mm);
+  block_lower_inverse(A, mm, keep, Linv, mm, mm);
+  __syncthreads();
+  for (int e = tid; e < mm * mm; e += nt) {           // T1 = S L⁻ᵀ
+    const int a = e / mm, b = e % mm;
+    double acc = 0.0;
+    for (int q = 0; q <= b; ++q) acc = fma(S[a * mm + q], Linv[b * mm + q], acc);
+    T1[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * mm; e += nt) {           // C = L⁻¹ T1
+    const int a = e / mm, b = e % mm;
+    double acc = 0.0;
+    for (int q = 0; q <= a; ++q) acc = fma(Linv[a * mm + q], T1[q * mm + b], acc);
+    C[e] = acc;
+  }
+  for (int e = tid; e < upto * mm; e += nt) {         // y_i = L⁻¹ (B t_i)
+    const int i = e / mm, a = e % mm;
+    double acc = 0.0;
+    for (int q = 0; q <= a; ++q) acc = fma(Linv[a * mm + q], G[(int64_t)q * g + mm + i], acc);
+    Y[e] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < upto; i += nt) {
+    double yy = 0.0;
+    for (int a = 0; a < mm; ++a) yy = fma(Y[i * mm + a], Y[i * mm + a], yy);
+    const double tt = G[(int64_t)(mm + i) * g + mm + i];
+    ratio[i] = tt > 0.0 ? sqrt(yy / tt) : 0.0;
+  }
+}
+
+// Kernel 2 (CTA i): Q = orthonormal basis of y_1 … y_{i−1} (modified Gram–Schmidt with one
+// re-orthogonalisation, residual < 1e-10 dropped — warp 0, a vector in registers, shuffle dots), then
+// M_i = P C P with P = I − QᵀQ as C − QᵀW' − W Q + Qᵀ H Q  (W = C Qᵀ, H = Q C Qᵀ), without forming P.
+constexpr int P3_VR = PPCA_MAX_M / 32;
+__global__ void __launch_bounds__(256) prop3_project_kernel(const double* __restrict__ C,
+                                                            const double* __restrict__ Y, int mm,
+                                                            double* __restrict__ Qg, double* __restrict__ Wg,
+                                                            double* __restrict__ Zg, double* __restrict__ Mg) {
+  const int i = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const size_t off = (size_t)i * mm * mm;
+  double* Q = Qg + off;   // nq × mm
+  double* W = Wg + off;   // mm × nq
+  double* Z = Zg + off;   // mm × nq
+  double* M = Mg + off;
+  __shared__ int nq_s;
+  if (tid < 32) {
+    const int lane = tid;
+    int nq = 0;
+    for (int j = 0; j < i; ++j) {
+      double w[P3_VR];
+#pragma unroll
+      for (int r = 0; r < P3_VR; ++r) {
+        const int a = lane + 32 * r;
+        w[r] = a < mm ? Y[j * mm + a] : 0.0;
+      }
+      for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < nq; ++q) {
+          double dot = 0.0;
+#pragma unroll
+          for (int r = 0; r < P3_VR; ++r) {
+            const int a = lane + 32 * r;
+            if (a < mm) dot = fma(Q[q * mm + a], w[r], dot);
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+#pragma unroll
+          for (int r = 0; r < P3_VR; ++r) {
+            const int a = lane + 32 * r;
+            if (a < mm) w[r] = fma(-dot, Q[q * mm + a], w[r]);
+          }
+        }
+      double nn = 0.0;
+#pragma unroll
+      for (int r = 0; r < P3_VR; ++r) nn = fma(w[r], w[r], nn);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+      const double nrm = sqrt(nn);
+      if (nrm >= 1e-10) {
+#pragma unroll
+        for (int r = 0; r < P3_VR; ++r) {
+          const int a = lane + 32 * r;
+          if (a < mm) Q[nq * mm + a] = w[r] / nrm;
+        }
+        ++nq;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) nq_s = nq;
+  }
+  __syncthreads();
+  const int nq = nq_s;
+  for (int e = tid; e < mm * nq; e += nt) {            // W = C Qᵀ  (mm × nq)
+    const int a = e / nq, r = e % nq;
+    double acc = 0.0;
+    for (int b = 0; b < mm; ++b) acc = fma(C[a * mm + b], Q[r * mm + b], acc);
+    W[e] = acc;
+  }
+  __syncthreads();
+  // Z = Qᵀ H with H = Q W (nq × nq): Z[a][s] = Σ_r Q[r][a] Σ_b Q[r][b] W[b][s]; computed as Z = Qᵀ(QW)
+  // with the inner product folded per (a, s) — O(mm²·nq²) but nq ≤ upto is small in practice
+  for (int e = tid; e < mm * nq; e += nt) {
+    const int a = e / nq, s2 = e % nq;
+    double acc = 0.0;
+    for (int r = 0; r < nq; ++r) {
+      double h = 0.0;
+      for (int b = 0; b < mm; ++b) h = fma(Q[r * mm + b], W[b * nq + s2], h);
+      acc = fma(Q[r * mm + a], h, acc);
+    }
+    Z[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * mm; e += nt) {            // M = C − QᵀWᵀ − W Q + Z Q
+    const int a = e / mm, b = e % mm;
+    double acc = C[e];
+    for (int r = 0; r < nq; ++r)
+      acc += -Q[r * mm + a] * W[b * nq + r] - W[a * nq + r] * Q[r * mm + b] + Z[a * nq + r] * Q[r * mm + b];
+    M[e] = acc;
+  }
+}
+
+// Kernel 3 (warp i): ∠(u_i, y_i) for u_i = row 0 of R_i (the top eigenvector of M_i), via
+// atan2(‖u − (u·ŷ)ŷ‖, |u·ŷ|) — accurate at tiny angles where acos is not.
+__global__ void prop3_angle_kernel(const double* __restrict__ R, const double* __restrict__ Y, int mm,
+                                   double* __restrict__ ang) {
+  const int i = blockIdx.x, lane = threadIdx.x;
+  const double* u = R + (size_t)i * mm * mm;
+  const double* y = Y + (size_t)i * mm;
+  double yy = 0.0, uy = 0.0;
+  for (int a = lane; a < mm; a += 32) {
+    yy = fma(y[a], y[a], yy);
+    uy = fma(u[a], y[a], uy);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    yy += __shfl_xor_sync(0xffffffffu, yy, o);
+    uy += __shfl_xor_sync(0xffffffffu, uy, o);
+  }
+  const double c = uy / sqrt(yy);                      // u·ŷ
+  double ss = 0.0;
+  for (int a = lane; a < mm; a += 32) {
+    const double r = u[a] - c * y[a] / sqrt(yy);
+    ss = fma(r, r, ss);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) ang[i] = atan2(sqrt(ss), fabs(c));
+}
+
+ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm, int upto, double* ratio_host,
+                         double* angles_host) {
+  const size_t m2 = (size_t)mm * mm;
+  double* w = (double*)scratch(c, S_P3, (7 * m2 + (size_t)upto * (5 * m2 + 2 * mm + 2) + 2 * mm + 64) * sizeof(double));
+  if (!w) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  double *A = w, *Linv = A + m2, *T1 = Linv + m2, *C = T1 + m2, *I = C + m2, *Y = I + m2;
+  double* ratio = Y + (size_t)upto * mm;
+  double* ang = ratio + upto;
+  double* Qg = ang + upto;
+  double* Wg = Qg + upto * m2;
+  double* Zg = Wg + upto * m2;
+  double* Mg = Zg + upto * m2;
+  double* Rg = Mg + upto * m2;
+  double* theta = Rg + upto * m2;
+  double* diag0 = theta + (size_t)upto * mm;
+  int* keep = (int*)(diag0 + mm);
+  prop3_coords_kernel<<<1, 256, 0, c->stream>>>(G, g, S, mm, upto, A, Linv, T1, C, I, Y, ratio, diag0, keep, c->d_err);
+  PPCA_LAUNCH_CHECK(c, "prop3_coords");
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(ratio_host, ratio, upto * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+                      "copy ratios"));
+  PPCA_TRY(finish(c, "ppca_check_prop3"));
+  for (int i = 0; i < upto; ++i)                       // DegenerateProjection
+    if (!(ratio_host[i] >= 1e-10))
+      return set_error(c, PPCA_ERR_DEGENERATE, "|pi_S(e_%d)| = %.3g |e_%d| < 1e-10", i + 1, ratio_host[i], i + 1);
+  prop3_project_kernel<<<upto, 256, 0, c->stream>>>(C, Y, mm, Qg, Wg, Zg, Mg);
+  PPCA_LAUNCH_CHECK(c, "prop3_project");
+  for (int i = 0; i < upto; ++i)                       // the variance maximiser on each complement
+    PPCA_TRY(ritz_solve(c, Mg + i * m2, I, mm, theta + (size_t)i * mm, Rg + i * m2, c->stream));
+  prop3_angle_kernel<<<upto, 32, 0, c->stream>>>(Rg, Y, mm, ang);
+  PPCA_LAUNCH_CHECK(c, "prop3_angle");
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(angles_host, ang, upto * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+                      "copy angles"));
+  return PPCA_OK;
+}
+
 }  // namespace ppca

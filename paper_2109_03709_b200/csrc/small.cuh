@@ -50,6 +50,11 @@ ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V,
                              int64_t d, double alpha, double mu);
 
 // dots[i] = <E_i, T_i> in fp64.
+// Prop. 3 checker (reading R28): from the stacked Gram G ([B; T], ld g) and S, the angles between π_S(t_i)
+// and the top eigenvector of the projected covariance on the complement of π_S(t_1..t_{i−1}); the ratios
+// ‖π_S(t_i)‖/‖t_i‖ come back first (DEGENERATE below 1e-10).  Synchronises the stream.
+ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm, int upto, double* ratio_host,
+                         double* angles_host);
 ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots);
 
 }  // namespace ppca
