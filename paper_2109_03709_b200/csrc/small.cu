@@ -897,18 +897,20 @@ __global__ void __launch_bounds__(256) prop3_coords_kernel(const double* __restr
 
 // Kernel 2 (CTA i): Q = orthonormal basis of y_1 … y_{i−1} (modified Gram–Schmidt with one
 // re-orthogonalisation, residual < 1e-10 dropped — warp 0, a vector in registers, shuffle dots), then
-// M_i = P C P with P = I − QᵀQ as C − QᵀW' − W Q + Qᵀ H Q  (W = C Qᵀ, H = Q C Qᵀ), without forming P.
+// M_i = P C P with P = I − QᵀQ as C − QᵀWᵀ − W Q + Z Q  (W = C Qᵀ, H = Q W, Z = Qᵀ H), without forming P.
 constexpr int P3_VR = PPCA_MAX_M / 32;
 __global__ void __launch_bounds__(256) prop3_project_kernel(const double* __restrict__ C,
                                                             const double* __restrict__ Y, int mm,
                                                             double* __restrict__ Qg, double* __restrict__ Wg,
-                                                            double* __restrict__ Zg, double* __restrict__ Mg) {
+                                                            double* __restrict__ Zg, double* __restrict__ Hg,
+                                                            double* __restrict__ Mg) {
   const int i = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const size_t off = (size_t)i * mm * mm;
   double* Q = Qg + off;   // nq × mm
   double* W = Wg + off;   // mm × nq
   double* Z = Zg + off;   // mm × nq
   double* M = Mg + off;
+  double* H = Hg + off;   // nq × nq
   __shared__ int nq_s;
   if (tid < 32) {
     const int lane = tid;
@@ -963,16 +965,17 @@ __global__ void __launch_bounds__(256) prop3_project_kernel(const double* __rest
     W[e] = acc;
   }
   __syncthreads();
-  // Z = Qᵀ H with H = Q W (nq × nq): Z[a][s] = Σ_r Q[r][a] Σ_b Q[r][b] W[b][s]; computed as Z = Qᵀ(QW)
-  // with the inner product folded per (a, s) — O(mm²·nq²) but nq ≤ upto is small in practice
-  for (int e = tid; e < mm * nq; e += nt) {
+  for (int e = tid; e < nq * nq; e += nt) {            // H = Q W  (nq × nq)
+    const int r = e / nq, s2 = e % nq;
+    double acc = 0.0;
+    for (int b = 0; b < mm; ++b) acc = fma(Q[r * mm + b], W[b * nq + s2], acc);
+    H[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < mm * nq; e += nt) {            // Z = Qᵀ H  (mm × nq)
     const int a = e / nq, s2 = e % nq;
     double acc = 0.0;
-    for (int r = 0; r < nq; ++r) {
-      double h = 0.0;
-      for (int b = 0; b < mm; ++b) h = fma(Q[r * mm + b], W[b * nq + s2], h);
-      acc = fma(Q[r * mm + a], h, acc);
-    }
+    for (int r = 0; r < nq; ++r) acc = fma(Q[r * mm + a], H[r * nq + s2], acc);
     Z[e] = acc;
   }
   __syncthreads();
@@ -1016,7 +1019,7 @@ __global__ void prop3_angle_kernel(const double* __restrict__ R, const double* _
 ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm, int upto, double* ratio_host,
                          double* angles_host) {
   const size_t m2 = (size_t)mm * mm;
-  double* w = (double*)scratch(c, S_P3, (7 * m2 + (size_t)upto * (5 * m2 + 2 * mm + 2) + 2 * mm + 64) * sizeof(double));
+  double* w = (double*)scratch(c, S_P3, (7 * m2 + (size_t)upto * (6 * m2 + 2 * mm + 2) + 2 * mm + 64) * sizeof(double));
   if (!w) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   double *A = w, *Linv = A + m2, *T1 = Linv + m2, *C = T1 + m2, *I = C + m2, *Y = I + m2;
   double* ratio = Y + (size_t)upto * mm;
@@ -1024,7 +1027,8 @@ ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm
   double* Qg = ang + upto;
   double* Wg = Qg + upto * m2;
   double* Zg = Wg + upto * m2;
-  double* Mg = Zg + upto * m2;
+  double* Hg = Zg + upto * m2;
+  double* Mg = Hg + upto * m2;
   double* Rg = Mg + upto * m2;
   double* theta = Rg + upto * m2;
   double* diag0 = theta + (size_t)upto * mm;
@@ -1037,7 +1041,7 @@ ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm
   for (int i = 0; i < upto; ++i)                       // DegenerateProjection
     if (!(ratio_host[i] >= 1e-10))
       return set_error(c, PPCA_ERR_DEGENERATE, "|pi_S(e_%d)| = %.3g |e_%d| < 1e-10", i + 1, ratio_host[i], i + 1);
-  prop3_project_kernel<<<upto, 256, 0, c->stream>>>(C, Y, mm, Qg, Wg, Zg, Mg);
+  prop3_project_kernel<<<upto, 256, 0, c->stream>>>(C, Y, mm, Qg, Wg, Zg, Hg, Mg);
   PPCA_LAUNCH_CHECK(c, "prop3_project");
   for (int i = 0; i < upto; ++i)                       // the variance maximiser on each complement
     PPCA_TRY(ritz_solve(c, Mg + i * m2, I, mm, theta + (size_t)i * mm, Rg + i * m2, c->stream));
