@@ -251,6 +251,77 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
   }
 }
 
+// No-drop Cholesky and L⁻¹ in one register-resident sweep (m ≤ 64; the power step's re-orthonormalisation).
+// Right-looking elimination on [A | M], M = I initially: at step j, with p = A_jj,
+//   A_ik −= A_ij A_kj / p  (i, k > j),   M_j· ← M_j· / √p,   M_i· −= (A_ij / p) M_j·  (i > j, M_j· unscaled),
+// so that M = L⁻¹ at the end (forward substitution of L Y = I, row-oriented).  Thread t owns row t/4 and the
+// columns ≡ t (mod 4) of both A and M (16 + 16 fp64 registers); column j of A and row j of M go through
+// double-buffered shared memory — one barrier per step, no index arithmetic in the loop (the blocked
+// shared-memory version's cost, tools/microbench_small.cu).  Rows/columns ≥ m are the identity.
+constexpr int CF_M = 64;
+static const bool g_chol_reg = !(getenv("PPCA_CHOL_REG") && atoi(getenv("PPCA_CHOL_REG")) == 0);
+__global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restrict__ G, int m,
+                                                           double* __restrict__ Linv, int* __restrict__ row_map,
+                                                           int* __restrict__ m_out, int* d_err) {
+  __shared__ double colb[2][CF_M];
+  __shared__ double rowb[2][CF_M];
+  const int t = threadIdx.x, i = t >> 2, cp = t & 3;
+  double a[16], mm_[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int k = cp + 4 * q;
+    a[q] = (i < m && k < m) ? G[i * m + k] : (i == k ? 1.0 : 0.0);
+    mm_[q] = i == k ? 1.0 : 0.0;
+  }
+  // step 0's buffers
+  if (cp == 0) colb[0][i] = a[0];
+  if (i == 0) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) rowb[0][cp + 4 * q] = mm_[q];
+  }
+  __syncthreads();
+  bool bad = false;
+  // fully unrolled: every register index is static, and the updates that only touch finished columns of A
+  // (k < j) or the zero upper triangle of M (c > j) are dropped at compile time
+#pragma unroll
+  for (int j = 0; j < CF_M; ++j) {
+    const int b = j & 1;
+    const double p = colb[b][j];
+    const bool ok = p > 0.0 && isfinite(p);
+    bad |= !ok;
+    const double r = ok ? rsqrt(p) : 0.0;
+    // row i > j: M_i −= (A_ij/p)·M_j;  row j: M_j ← r·M_j = M_j − (1 − r)·M_j (rowb holds M_j);  rows < j: 0.
+    // colb rows < j are published as zero, so f needs no mask there.
+    const double f = i == j ? 1.0 - r : colb[b][i] * (r * r);
+    const double fa = i > j ? f : 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (4 * q + 3 > j) a[q] = fma(-fa, colb[b][cp + 4 * q], a[q]);
+      if (4 * q <= j) mm_[q] = fma(-f, rowb[b][cp + 4 * q], mm_[q]);
+    }
+    if (j + 1 < CF_M) {                              // publish column j+1 of A and row j+1 of M
+      const int jn = j + 1, nb = b ^ 1;
+      if (cp == (jn & 3)) colb[nb][i] = i >= jn ? a[jn >> 2] : 0.0;
+      if (i == jn) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (4 * q <= jn) rowb[nb][cp + 4 * q] = mm_[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && t == 0) atomicOr(d_err, DEV_COLLAPSE);
+  if (i < m) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k = cp + 4 * q;
+      if (k < m) Linv[i * m + k] = mm_[q];
+    }
+  }
+  if (t < m) row_map[t] = t;
+  if (t == 0) *m_out = m;
+}
+
 static size_t chol_inv_smem(int m) {
   const int lda = m | 1;
   return (size_t)m * lda * sizeof(double) + m * sizeof(double) + ((m + 1) & ~1) * sizeof(int) +
@@ -320,8 +391,12 @@ ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_m
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const size_t smem = chol_inv_smem(m);
-  chol_inv_kernel<<<1, 256, smem, st>>>(G, m, 0.0, Linv, row_map, m_out, c->d_err);
+  if (m <= CF_M && g_chol_reg) {
+    chol_inv_reg_kernel<<<1, 256, 0, st>>>(G, m, Linv, row_map, m_out, c->d_err);
+  } else {
+    const size_t smem = chol_inv_smem(m);
+    chol_inv_kernel<<<1, 256, smem, st>>>(G, m, 0.0, Linv, row_map, m_out, c->d_err);
+  }
   PPCA_LAUNCH_CHECK(c, "chol_inv");
   return PPCA_OK;
 }
@@ -354,7 +429,10 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   const size_t smem = chol_inv_smem(m);
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
     PPCA_TRY(vec_gram(c, Zin, m, d, G));
-    chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
+    if (m <= CF_M && g_chol_reg)
+      chol_inv_reg_kernel<<<1, 256, 0, c->stream>>>(G, m, Linv, row_map, d_mout, c->d_err);
+    else
+      chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
     PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, Zin, d, W, c->stream));
     if (m_out) *m_out = m;
