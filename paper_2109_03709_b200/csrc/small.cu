@@ -254,22 +254,25 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
 // No-drop Cholesky and L⁻¹ in one register-resident sweep (m ≤ 64; the power step's re-orthonormalisation).
 // Right-looking elimination on [A | M], M = I initially: at step j, with p = A_jj,
 //   A_ik −= A_ij A_kj / p  (i, k > j),   M_j· ← M_j· / √p,   M_i· −= (A_ij / p) M_j·  (i > j, M_j· unscaled),
-// so that M = L⁻¹ at the end (forward substitution of L Y = I, row-oriented).  Thread t owns row t/4 and the
-// columns ≡ t (mod 4) of both A and M (16 + 16 fp64 registers); column j of A and row j of M go through
+// so that M = L⁻¹ at the end (forward substitution of L Y = I, row-oriented).  Thread t owns row t/CQ and the
+// columns ≡ t (mod CQ) of both A and M (64/CQ + 64/CQ fp64 registers; CQ = 8, 512 threads: 21 µs in ncu
+// against 29 µs for CQ = 4 and 27 µs for CQ = 16); column j of A and row j of M go through
 // double-buffered shared memory — one barrier per step, no index arithmetic in the loop (the blocked
 // shared-memory version's cost, tools/microbench_small.cu).  Rows/columns ≥ m are the identity.
 constexpr int CF_M = 64;
 static const bool g_chol_reg = !(getenv("PPCA_CHOL_REG") && atoi(getenv("PPCA_CHOL_REG")) == 0);
-__global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restrict__ G, int m,
+template <int CQ>
+__global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
                                                            double* __restrict__ Linv, int* __restrict__ row_map,
                                                            int* __restrict__ m_out, int* d_err) {
   __shared__ double colb[2][CF_M];
   __shared__ double rowb[2][CF_M];
-  const int t = threadIdx.x, i = t >> 2, cp = t & 3;
-  double a[16], mm_[16];
+  constexpr int NQ = CF_M / CQ;
+  const int t = threadIdx.x, i = t / CQ, cp = t % CQ;
+  double a[NQ], mm_[NQ];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int k = cp + 4 * q;
+  for (int q = 0; q < NQ; ++q) {
+    const int k = cp + CQ * q;
     a[q] = (i < m && k < m) ? G[i * m + k] : (i == k ? 1.0 : 0.0);
     mm_[q] = i == k ? 1.0 : 0.0;
   }
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
   if (cp == 0) colb[0][i] = a[0];
   if (i == 0) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) rowb[0][cp + 4 * q] = mm_[q];
+    for (int q = 0; q < NQ; ++q) rowb[0][cp + CQ * q] = mm_[q];
   }
   __syncthreads();
   bool bad = false;
@@ -295,17 +298,17 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
     const double f = i == j ? 1.0 - r : colb[b][i] * (r * r);
     const double fa = i > j ? f : 0.0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      if (4 * q + 3 > j) a[q] = fma(-fa, colb[b][cp + 4 * q], a[q]);
-      if (4 * q <= j) mm_[q] = fma(-f, rowb[b][cp + 4 * q], mm_[q]);
+    for (int q = 0; q < NQ; ++q) {
+      if (CQ * q + CQ - 1 > j) a[q] = fma(-fa, colb[b][cp + CQ * q], a[q]);
+      if (CQ * q <= j) mm_[q] = fma(-f, rowb[b][cp + CQ * q], mm_[q]);
     }
     if (j + 1 < CF_M) {                              // publish column j+1 of A and row j+1 of M
       const int jn = j + 1, nb = b ^ 1;
-      if (cp == (jn & 3)) colb[nb][i] = i >= jn ? a[jn >> 2] : 0.0;
+      if (cp == jn % CQ) colb[nb][i] = i >= jn ? a[jn / CQ] : 0.0;
       if (i == jn) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (4 * q <= jn) rowb[nb][cp + 4 * q] = mm_[q];
+        for (int q = 0; q < NQ; ++q)
+          if (CQ * q <= jn) rowb[nb][cp + CQ * q] = mm_[q];
       }
     }
     __syncthreads();
@@ -313,13 +316,24 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
   if (bad && t == 0) atomicOr(d_err, DEV_COLLAPSE);
   if (i < m) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int k = cp + 4 * q;
+    for (int q = 0; q < NQ; ++q) {
+      const int k = cp + CQ * q;
       if (k < m) Linv[i * m + k] = mm_[q];
     }
   }
   if (t < m) row_map[t] = t;
   if (t == 0) *m_out = m;
+}
+
+static int g_chol_cq = getenv("PPCA_CHOL_CQ") ? atoi(getenv("PPCA_CHOL_CQ")) : 8;
+static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_map, int* m_out, int* d_err,
+                                cudaStream_t st) {
+  if (g_chol_cq == 4)
+    chol_inv_reg_kernel<4><<<1, 256, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
+  else if (g_chol_cq == 16)
+    chol_inv_reg_kernel<16><<<1, 1024, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
+  else
+    chol_inv_reg_kernel<8><<<1, 512, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
 }
 
 static size_t chol_inv_smem(int m) {
@@ -392,7 +406,7 @@ ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_m
     attr = true;
   }
   if (m <= CF_M && g_chol_reg) {
-    chol_inv_reg_kernel<<<1, 256, 0, st>>>(G, m, Linv, row_map, m_out, c->d_err);
+    launch_chol_inv_reg(G, m, Linv, row_map, m_out, c->d_err, st);
   } else {
     const size_t smem = chol_inv_smem(m);
     chol_inv_kernel<<<1, 256, smem, st>>>(G, m, 0.0, Linv, row_map, m_out, c->d_err);
@@ -430,7 +444,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
     PPCA_TRY(vec_gram(c, Zin, m, d, G));
     if (m <= CF_M && g_chol_reg)
-      chol_inv_reg_kernel<<<1, 256, 0, c->stream>>>(G, m, Linv, row_map, d_mout, c->d_err);
+      launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
       chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
@@ -443,8 +457,11 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
                         "copy Z"));
   for (int pass = 0; pass < passes; ++pass) {
     PPCA_TRY(vec_gram(c, W, m, d, G));
-    chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, pass == 0 ? drop_tol : 0.0, Linv, row_map, d_mout,
-                                                 c->d_err);
+    const double dt = pass == 0 ? drop_tol : 0.0;
+    if (dt <= 0.0 && m <= CF_M && g_chol_reg)
+      launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
+    else
+      chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, dt, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
     if (pass == 0 && drop_tol > 0.0) {
       int h_m = m;
