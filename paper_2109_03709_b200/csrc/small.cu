@@ -351,12 +351,13 @@ constexpr int AP_COLS = 32;
 __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
-                                                         int64_t d, float* __restrict__ OUT) {
-  extern __shared__ double cs[];                 // rows × m_in (fp64), then m_in × AP_COLS (fp32)
-  float* ins = reinterpret_cast<float*>(cs + (size_t)rows * m_in);
+                                                         int64_t d, float* __restrict__ OUT, int rows_per_cta) {
+  extern __shared__ double cs[];                 // this CTA's rows × m_in (fp64), then m_in × AP_COLS (fp32)
+  const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  float* ins = reinterpret_cast<float*>(cs + (size_t)rows_per_cta * m_in);
   const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
-  copy_batched<16>(threadIdx.x, rows * m_in, blockDim.x,
-                   [&](int64_t e) { return C[(e / m_in) * ldc + e % m_in]; },
+  copy_batched<16>(threadIdx.x, (r1 - r0) * m_in, blockDim.x,
+                   [&](int64_t e) { return C[(r0 + e / m_in) * ldc + e % m_in]; },
                    [&](int64_t e, double v) { cs[e] = v; });
   copy_batched<8>(threadIdx.x, m_in * AP_COLS, blockDim.x,
                   [&](int64_t e) {
@@ -367,10 +368,10 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t x = x0 + lane;
-  for (int i = warp; i < rows; i += 8) {
+  for (int i = r0 + warp; i < r1; i += 8) {
     const int oi = row_map ? row_map[i] : i;
     if (oi < 0) continue;
-    const double* crow = cs + (size_t)i * m_in;
+    const double* crow = cs + (size_t)(i - r0) * m_in;
     const int jend = lower ? min(i + 1, m_in) : m_in;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: the FMA latency is hidden
     int j = 0;
@@ -392,8 +393,17 @@ static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_
     cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  size_t smem = (size_t)rows * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
-  apply_rows_kernel<<<(unsigned)ceil_div(d, AP_COLS), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
+  // row blocks (multiples of 8 rows) until the grid covers the SMs: d = 1024 alone gives 32 CTAs
+  const int64_t gx = ceil_div(d, (int64_t)AP_COLS);
+  static const bool split = !(getenv("PPCA_APPLY_SPLIT") && atoi(getenv("PPCA_APPLY_SPLIT")) == 0);
+  int rpc = rows;
+  if (split && gx < c->sm_count) {
+    const int gy = (int)std::min<int64_t>(ceil_div((int64_t)c->sm_count, gx), ceil_div((int64_t)rows, (int64_t)8));
+    rpc = (int)ceil_div((int64_t)ceil_div((int64_t)rows, (int64_t)gy), (int64_t)8) * 8;
+  }
+  const unsigned gy = (unsigned)ceil_div((int64_t)rows, (int64_t)rpc);
+  size_t smem = (size_t)rpc * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
+  apply_rows_kernel<<<dim3((unsigned)gx, gy), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
