@@ -204,12 +204,17 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
 
   // 1. L = chol(B), L⁻¹, C = L⁻¹ S L⁻ᵀ (symmetrised)
   if (tid == 0) g_ritz_clk[0] = clock64();
-  ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return Bm[e]; }, [&](int64_t e, double v) { A[e] = v; });
-  __syncthreads();
-  ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err, m);
-  if (tid == 0) g_ritz_clk[1] = clock64();
-  ppca::block_lower_inverse(A, m, keep, Linv, m, m);
-  if (tid == 0) g_ritz_clk[2] = clock64();
+  if (m <= 64 && nt == 512) {                        // register sweep (small.cu): Cholesky and L⁻¹ together
+    ppca::chol_inv_sweep<8>(Bm, m, Linv, m, keep, d_err);
+    if (tid == 0) g_ritz_clk[1] = g_ritz_clk[2] = clock64();
+  } else {
+    ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return Bm[e]; }, [&](int64_t e, double v) { A[e] = v; });
+    __syncthreads();
+    ppca::block_cholesky(A, m, 0.0, keep, diag0, d_err, m);
+    if (tid == 0) g_ritz_clk[1] = clock64();
+    ppca::block_lower_inverse(A, m, keep, Linv, m, m);
+    if (tid == 0) g_ritz_clk[2] = clock64();
+  }
   ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return S[e]; }, [&](int64_t e, double v) { A[e] = v; });
   __syncthreads();
   for (int e = tid; e < m * m; e += nt) {

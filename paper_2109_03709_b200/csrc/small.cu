@@ -261,10 +261,12 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
 // shared-memory version's cost, tools/microbench_small.cu).  Rows/columns ≥ m are the identity.
 constexpr int CF_M = 64;
 static const bool g_chol_reg = !(getenv("PPCA_CHOL_REG") && atoi(getenv("PPCA_CHOL_REG")) == 0);
+// the sweep as a block-level device function (blockDim.x == 64·CQ): G [m][m] and Linv [m][ldl] in any
+// memory space; keep[i] = 1 (no drops); a non-positive pivot flags DEV_COLLAPSE.  Used by the CholQR kernel
+// below and by the Ritz kernels (ritz.cuh) for the operand Gram's L⁻¹.
 template <int CQ>
-__global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
-                                                           double* __restrict__ Linv, int* __restrict__ row_map,
-                                                           int* __restrict__ m_out, int* d_err) {
+__device__ void chol_inv_sweep(const double* __restrict__ G, int m, double* __restrict__ Linv, int ldl,
+                               int* __restrict__ keep, int* d_err) {
   __shared__ double colb[2][CF_M];
   __shared__ double rowb[2][CF_M];
   constexpr int NQ = CF_M / CQ;
@@ -318,11 +320,20 @@ __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __r
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int k = cp + CQ * q;
-      if (k < m) Linv[i * m + k] = mm_[q];
+      if (k < m) Linv[i * ldl + k] = mm_[q];
     }
   }
-  if (t < m) row_map[t] = t;
-  if (t == 0) *m_out = m;
+  if (keep && t < m) keep[t] = 1;
+  __syncthreads();
+}
+
+template <int CQ>
+__global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
+                                                           double* __restrict__ Linv, int* __restrict__ row_map,
+                                                           int* __restrict__ m_out, int* d_err) {
+  chol_inv_sweep<CQ>(G, m, Linv, m, nullptr, d_err);
+  if (threadIdx.x < m) row_map[threadIdx.x] = threadIdx.x;
+  if (threadIdx.x == 0) *m_out = m;
 }
 
 static int g_chol_cq = getenv("PPCA_CHOL_CQ") ? atoi(getenv("PPCA_CHOL_CQ")) : 8;
