@@ -109,7 +109,10 @@ int ppca_abi_version(void);
 ppca_status ppca_get_unique_id(void* uid_out);
 
 /* device: CUDA ordinal; stream: cudaStream_t or NULL (legacy default stream);
- * uid: PPCA_UNIQUE_ID_BYTES host bytes (required if world > 1, ignored otherwise). */
+ * uid: PPCA_UNIQUE_ID_BYTES host bytes, required if world > 1.  With world == 1 a non-NULL uid creates a
+ * one-rank NCCL communicator, so the collective call sites run on one GPU as well (tests); NULL: none.
+ * Errors: INVALID_ARG, UNSUPPORTED (not sm_100 / NCCL missing), NCCL (CommInitRank failed or the
+ * communicator's rank count differs from world), CUDA. */
 ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank, int world,
                             ppca_ctx** out);
 ppca_status ppca_ctx_destroy(ppca_ctx* ctx);
@@ -117,6 +120,11 @@ ppca_status ppca_ctx_destroy(ppca_ctx* ctx);
 ppca_status ppca_last_error(const ppca_ctx* ctx, char* msg, size_t cap);
 /* Number of library kernel launches enqueued by this context since creation (bench evidence). */
 int64_t ppca_launch_count(const ppca_ctx* ctx);
+/* Number of NCCL operations (one grouped [Z|S] all-reduce counts once) enqueued since creation. */
+int64_t ppca_collective_count(const ppca_ctx* ctx);
+/* 1 if this build reads experiment switches from the environment (-DPPCA_EXPERIMENTS), 0 for the
+ * shipped library (bench.py asserts 0: no environment variable can change or skip its work). */
+int ppca_experiments_enabled(void);
 
 /* ---------------------------------------------------------------- hot path */
 
@@ -135,10 +143,15 @@ ppca_status ppca_split_f32(ppca_ctx* ctx, void* X, int64_t n_local, int64_t d, i
  * per iteration Y = X·Wᵀ, Z = YᵀX (fused streaming pass over X), all-reduce, W ← orth(Z)
  * (Q-factor with positive diag R).  W: device [m][d] in/out.  init_seed != 0 initialises W
  * from N(0,1) draws (Philox stream 6) then orthonormalises; init_seed == 0 resumes from W.
+ * iters: the iteration budget (BASELINE fixes 20/50/30, reading R13).
+ * eps > 0: the paper's stop rule "terminates when ‖x_i − x_{i+1}‖ < ε" (P L61-62), applied to the
+ * block as max_j ‖w_j^{t+1} − s_j w_j^t‖ < eps with s_j = sign⟨w_j^{t+1}, w_j^t⟩ (columns are defined up
+ * to sign); checking it costs one host synchronisation per iteration.  eps <= 0: run all iters.
  * theta_hist_host: optional host double[iters*m]: row t holds the pPCA (Rayleigh–Ritz)
- * eigenvalue estimates of span(W_t) computed from the same pass (S_t = YᵀY), descending. */
-ppca_status ppca_prime_power(ppca_ctx* ctx, const ppca_matrix* X, int m, int iters,
-                             uint64_t init_seed, float* W, double* theta_hist_host);
+ * eigenvalue estimates of span(W_t) computed from the same pass (S_t = YᵀY), descending; rows past
+ * the stop are zero.  iters_done (optional): iterations run. */
+ppca_status ppca_prime_power(ppca_ctx* ctx, const ppca_matrix* X, int m, int iters, double eps,
+                             uint64_t init_seed, float* W, double* theta_hist_host, int* iters_done);
 
 /* Generalised Oja / Sanger minibatch priming (§2.2; Nesterov L326):
  * G = X_bᵀY_b − W·triu(Y_bᵀY_b) summed over the global minibatch (reading R8), v ← μv + G,
@@ -168,7 +181,8 @@ ppca_status ppca_refine(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int
 /* Row-subsampled pPCA refinement (§5.2: "we only project 10% of the data for computing
  * full-PCA"; reading R25): as ppca_refine, but the projected covariance
  * is formed from the 128-row tiles of each shard whose Philox4x32-10 uniform (sample_seed, stream 7,
- * key = global tile index for CONTIGUOUS shards) is below `fraction`, and θ are rescaled by
+ * key = the global index of the tile's first row for CONTIGUOUS shards; tiles are cut from each shard's
+ * first row) is below `fraction`, and θ are rescaled by
  * n_global / rows used (an estimate of XᵀX's eigenvalues).  fraction ≥ 1 is ppca_refine.
  * rows_used (optional): rows in the sample over all ranks.  An empty sample is INVALID_ARG. */
 ppca_status ppca_refine_sampled(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k,
@@ -194,6 +208,15 @@ ppca_status ppca_check_prop3(ppca_ctx* ctx, const ppca_matrix* X, const float* V
  * E, T: device [k][d] unit rows.  angles_host: double[k]; lces_host: int[nthr]. */
 ppca_status ppca_eval(ppca_ctx* ctx, const float* E, const float* T, int k, int64_t d,
                       const double* thr_host, int nthr, double* angles_host, int* lces_host);
+
+/* Certification support for the reference of large configs (reading R29):
+ * res_host[i] = ‖XᵀX e_i − θ_i e_i‖₂ for the k rows e_i of E (device [k][d] fp32, unit rows) and
+ * theta_host[i] (host double[k]).  By Weyl some eigenvalue of XᵀX lies within res_i of θ_i; with a gap δ
+ * the angle to the true eigenvector is ≤ res_i/δ (Davis–Kahan).  One exact-fp32 CUDA-core pass over X
+ * (no bf16 rounding of E or of X·Eᵀ), fp64 split-K sums, summed over ranks.  Untimed support, not a
+ * step of the method.  Errors: INVALID_ARG (null pointers), as ppca_refine for X, k ≤ min(d, 128). */
+ppca_status ppca_ritz_residuals(ppca_ctx* ctx, const ppca_matrix* X, const float* E, int k,
+                                const double* theta_host, double* res_host);
 
 /* Captured variance vᵀ(XᵀX)v = ‖Xv‖² for each row of V (PAPER.md L416 footnote),
  * summed over ranks.  var_host: double[m]. */

@@ -81,6 +81,18 @@ def uniforms(seed: int, stream: int, first: int, count: int) -> np.ndarray:
     return (words(seed, stream, first, count).astype(np.float64) + 0.5) * 2.0 ** -32
 
 
+def uniforms_at(seed: int, stream: int, idx) -> np.ndarray:
+    """U at arbitrary element indices idx (uint64-compatible array) of (seed, stream)."""
+    idx = np.asarray(idx, dtype=np.uint64).reshape(-1)
+    if idx.size == 0:
+        return np.zeros(0)
+    calls = idx >> np.uint64(2)
+    r = philox4x32_10(calls & _MASK32, calls >> np.uint64(32), np.uint32(stream), np.uint32(0),
+                      np.uint32(seed & 0xFFFFFFFF), np.uint32((seed >> 32) & 0xFFFFFFFF))
+    w = np.stack(r, axis=1)[np.arange(idx.size), (idx & np.uint64(3)).astype(np.int64)]
+    return (w.astype(np.float64) + 0.5) * 2.0 ** -32
+
+
 def gaussians(seed: int, stream: int, first: int, count: int) -> np.ndarray:
     """Box-Muller on word pairs (2j, 2j+1): z_{2j} = r cos(2πu_{2j+1}), z_{2j+1} = r sin(2πu_{2j+1}),
     r = sqrt(-2 ln u_{2j}).  Element e depends only on pair e // 2."""

@@ -154,14 +154,26 @@ def power_step(X: np.ndarray, W: np.ndarray):
     return W_new, S
 
 
-def prime_power(X: np.ndarray, W0_raw: np.ndarray, iters: int):
-    """Block power priming: W_0 = GS(normalised Gaussians), then `iters` power steps.
-    Returns (W_iters, [S_0 … S_{iters-1}])."""
+def column_moves(W_new: np.ndarray, W_old: np.ndarray) -> np.ndarray:
+    """‖x_{i+1} − x_i‖ of the stop rule (P L61-62) for every column of the block, sign-aligned: a column is
+    an eigen-direction estimate defined up to sign, so min(‖w' − w‖, ‖w' + w‖)."""
+    return np.array([min(np.linalg.norm(W_new[j] - W_old[j]), np.linalg.norm(W_new[j] + W_old[j]))
+                     for j in range(W_new.shape[0])])
+
+
+def prime_power(X: np.ndarray, W0_raw: np.ndarray, iters: int, eps: float = 0.0):
+    """Block power priming: W_0 = GS(normalised Gaussians), then at most `iters` power steps.  eps > 0: the
+    power method "terminates when ‖x_i − x_{i+1}‖ < ε" (P L61-62), here once every column moved less than
+    eps (column_moves).  Returns (W_final, [S_0 … S_{t-1}]) — one S per iteration run."""
     W = gram_schmidt(init_vectors(W0_raw), drop=False)
     S_hist = []
     for _ in range(iters):
-        W, S = power_step(X, W)
+        W_new, S = power_step(X, W)
         S_hist.append(S)
+        moved = column_moves(W_new, W)
+        W = W_new
+        if eps > 0 and np.max(moved) < eps:
+            break
     return W, S_hist
 
 
@@ -285,10 +297,11 @@ STREAM_SAMPLE = 7          # Philox stream of the row-tile sample (R25)
 
 def sampled_rows(n: int, fraction: float, seed: int) -> np.ndarray:
     """R25 (P L378 "we only project 10% of the data"): the row blocks [128t, 128t+128) ∩ [0, n) whose
-    uniform U(seed, stream 7, t) is below `fraction` (the random numbers are inputs: inputs.philox)."""
+    uniform U(seed, stream 7, key = 128t, the global index of the block's first row) is below `fraction`
+    (the random numbers are inputs: inputs.philox)."""
     from inputs import philox as ph
     nt = -(-n // SAMPLE_TILE)
-    u = ph.uniforms(seed, STREAM_SAMPLE, 0, nt)
+    u = ph.uniforms_at(seed, STREAM_SAMPLE, np.arange(nt, dtype=np.uint64) * SAMPLE_TILE)
     keep = np.nonzero(u < fraction)[0]
     if keep.size == 0:
         return np.zeros(0, dtype=np.int64)
@@ -403,9 +416,66 @@ def truth(X: np.ndarray):
 
 
 def subspace_error(E: np.ndarray, T: np.ndarray) -> float:
-    """‖(I − T_kᵀT_k) E_kᵀ‖₂ for row-orthonormal E_k, T_k (sine of the largest principal angle)."""
+    """Subspace error of SURVEY §8(c) O8 / reading R20 (the C5 target): ‖(I − T_kᵀT_k) E_kᵀ‖₂ for
+    row-orthonormal E_k, T_k [k][d] — the sine of the largest principal angle between span E and span T."""
     P = E.T - T.T @ (T @ E.T)
     return float(np.linalg.norm(P, 2))
+
+
+def ritz_residuals(X: np.ndarray, E: np.ndarray, theta: np.ndarray) -> np.ndarray:
+    """r_i = ‖XᵀX e_i − θ_i e_i‖₂ for the rows e_i of E, with XᵀX applied as Xᵀ(X e_i) (never formed):
+    the quantity the Weyl / Davis–Kahan certificates of certified_top are built on (reading R29)."""
+    X = np.asarray(X, dtype=np.float64)
+    E = np.asarray(E, dtype=np.float64)
+    ME = (X @ E.T).T @ X
+    R = ME - np.asarray(theta, dtype=np.float64)[:, None] * E
+    return np.sqrt(np.sum(R * R, axis=1))
+
+
+def certified_top(X: np.ndarray, k: int, W0_raw: np.ndarray, max_iters: int = 500, rtol: float = 1e-9):
+    """Residual-certified reference for the top-k eigenpairs of M = XᵀX when M is too large to form (SURVEY
+    §8(c) O9; reading R29): block power iteration (P L61-63) on m = W0_raw.shape[0] > k vectors with a
+    Rayleigh–Ritz step each iteration (Alg. 1, P L47-51), fp64, until every residual
+    r_i = ‖M e_i − θ_i e_i‖ (i ≤ k) is ≤ rtol·θ_1 or max_iters.  One pass over X per iteration gives both the
+    residuals of the current Ritz pairs and the next iterate (span M·E = span M·W).
+    Bounds (returned, R29):
+      weyl_i  = r_i                      — some eigenvalue of M lies in [θ_i − r_i, θ_i + r_i] (Weyl);
+      gap_i   = min_{j≠i, j≤m} |θ_i − θ_j| − r_j, and θ_i − (θ_m + r_m) for the unresolved tail
+                (assumes the m Ritz intervals hold the top-m eigenvalues: block power from a random start);
+      angle_i = r_i / gap_i              — sin∠(e_i, true eigenvector i) (Davis–Kahan);
+      subspace = ‖R_k‖₂ / δ, δ = θ_k − (θ_{k+1} + r_{k+1})  — sin of the largest principal angle between
+                span E_k and the true top-k subspace (Davis–Kahan sinΘ).
+    Returns a dict with theta, E (rows, sign convention), res, gap, angle_bound, subspace_bound, iters."""
+    X = np.asarray(X, dtype=np.float64)
+    m = W0_raw.shape[0]
+    if not k < m:
+        raise OracleError("certified_top needs m > k (the tail gap uses theta_{k+1})")
+    W = gram_schmidt(init_vectors(W0_raw), drop=False)
+    out = None
+    for it in range(1, max_iters + 1):
+        Y = X @ W.T                                        # one pass: Y = X Wᵀ …
+        S = Y.T @ Y                                        # … S = W M Wᵀ
+        w, U = np.linalg.eigh(S)                           # Rayleigh–Ritz (library eigensolver as a step)
+        order = np.argsort(-w, kind="stable")
+        theta, U = w[order], U[:, order].T                 # rows of U: eigenvectors of S
+        E = U @ W                                          # Ritz vectors (orthonormal rows)
+        ME = (Y @ U.T).T @ X                               # rows: (M e_i)ᵀ = (X e_i)ᵀ X
+        R = ME - theta[:, None] * E                        # residual rows
+        res = np.sqrt(np.sum(R * R, axis=1))
+        out = (theta, E, R, res, it)
+        if np.all(res[:k] <= rtol * theta[0]):
+            break
+        W = gram_schmidt(ME, drop=False)                   # next iterate: span(M E) = span(M W)
+    theta, E, R, res, it = out
+    gap = np.empty(k)
+    for i in range(k):
+        others = [abs(theta[i] - theta[j]) - res[j] for j in range(m) if j != i]
+        gap[i] = min(min(others), theta[i] - (theta[m - 1] + res[m - 1]))
+    delta = theta[k - 1] - (theta[k] + res[k])
+    sub = float(np.linalg.norm(R[:k], 2)) / delta if delta > 0 else math.inf
+    ang = np.where(gap > 0, res[:k] / np.where(gap > 0, gap, 1.0), math.inf)
+    return {"theta": theta[:k], "E": sign_convention(E[:k]), "res": res[:k], "gap": gap,
+            "angle_bound": ang, "subspace_bound": sub, "iters": it, "theta_all": theta, "res_all": res}
 
 
 def relative_gaps(lam: np.ndarray) -> np.ndarray:

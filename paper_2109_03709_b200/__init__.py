@@ -31,7 +31,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
            "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
-           "ppca_check_prop3"]
+           "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals"]
 
 
 class PPCAError(RuntimeError):
@@ -76,7 +76,10 @@ def load(path: str = LIB_PATH):
         "ppca_last_error": (I, [P, ctypes.c_char_p, ctypes.c_size_t]),
         "ppca_launch_count": (I64, [P]),
         "ppca_generate": (I, [P, ctypes.POINTER(ppca_gen_spec), P, I64, ctypes.POINTER(I64), P]),
-        "ppca_prime_power": (I, [P, ctypes.POINTER(ppca_matrix), I, I, ctypes.c_uint64, P, P]),
+        "ppca_prime_power": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, ctypes.c_uint64, P, P, ctypes.POINTER(I)]),
+        "ppca_collective_count": (I64, [P]),
+        "ppca_ritz_residuals": (I, [P, ctypes.POINTER(ppca_matrix), P, I, P, P]),
+        "ppca_experiments_enabled": (I, []),
         "ppca_prime_oja": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, D, I64, ctypes.c_uint64, P, P,
                                ctypes.POINTER(I64)]),
         "ppca_prime_eigengame": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, D, I64, ctypes.c_uint64, P, P,
@@ -231,6 +234,20 @@ def ppca_launch_count(ctx) -> int:
     return int(load().ppca_launch_count(ctx))
 
 
+def ppca_collective_count(ctx) -> int:
+    return int(load().ppca_collective_count(ctx))
+
+
+def ppca_experiments_enabled() -> bool:
+    return bool(load().ppca_experiments_enabled())
+
+
+def ppca_ctx_create_one_rank_comm(device: int = 0, stream=None):
+    """A world-1 context WITH a one-rank NCCL communicator: every all-reduce call site of the path runs
+    (tests of the multi-GPU data plane on one GPU)."""
+    return ppca_ctx_create(device, stream, ppca_get_unique_id(), 0, 1)
+
+
 def ppca_set_pass_impl(ctx, impl: int) -> None:
     _check(ctx, load().ppca_set_pass_impl(ctx, impl), "ppca_set_pass_impl")
 
@@ -273,11 +290,20 @@ def ppca_split_f32(ctx, X, d: int | None = None) -> None:
                                       X.stride(0)), "ppca_split_f32")
 
 
-def ppca_prime_power(ctx, X: ppca_matrix, m: int, iters: int, init_seed: int, W, theta_hist: bool = False):
+def ppca_prime_power_ex(ctx, X: ppca_matrix, m: int, iters: int, init_seed: int, W, theta_hist: bool = False,
+                        eps: float = 0.0):
+    """Block power priming with the paper's stop rule (eps > 0, P L61-62): (θ history rows run | None,
+    iterations run)."""
     th = np.zeros((max(iters, 1), m), dtype=np.float64) if theta_hist else None
-    _check(ctx, load().ppca_prime_power(ctx, ctypes.byref(X), m, iters, init_seed, _ptr(W),
-                                        _np_ptr(th) if th is not None else None), "ppca_prime_power")
-    return th[:iters] if th is not None else None
+    done = ctypes.c_int()
+    _check(ctx, load().ppca_prime_power(ctx, ctypes.byref(X), m, iters, float(eps), init_seed, _ptr(W),
+                                        _np_ptr(th) if th is not None else None, ctypes.byref(done)),
+           "ppca_prime_power")
+    return (th[:done.value] if th is not None else None), done.value
+
+
+def ppca_prime_power(ctx, X: ppca_matrix, m: int, iters: int, init_seed: int, W, theta_hist: bool = False):
+    return ppca_prime_power_ex(ctx, X, m, iters, init_seed, W, theta_hist)[0]
 
 
 def ppca_prime_oja(ctx, X: ppca_matrix, m: int, batch: int, alpha: float, momentum: float, steps: int,
@@ -332,6 +358,15 @@ def ppca_eval(ctx, E, T, k: int, d: int, thresholds) -> tuple[np.ndarray, np.nda
     _check(ctx, load().ppca_eval(ctx, _ptr(E), _ptr(T), k, d, _np_ptr(thr), len(thr), _np_ptr(ang), _np_ptr(lc)),
            "ppca_eval")
     return ang, lc
+
+
+def ppca_ritz_residuals(ctx, X: ppca_matrix, E, k: int, theta) -> np.ndarray:
+    """‖XᵀX e_i − θ_i e_i‖ for the rows of E (certification support, reading R29)."""
+    th = np.ascontiguousarray(theta[:k], dtype=np.float64)
+    out = np.zeros(k, dtype=np.float64)
+    _check(ctx, load().ppca_ritz_residuals(ctx, ctypes.byref(X), _ptr(E), k, _np_ptr(th), _np_ptr(out)),
+           "ppca_ritz_residuals")
+    return out
 
 
 def ppca_captured_variance(ctx, X: ppca_matrix, V, m: int) -> np.ndarray:

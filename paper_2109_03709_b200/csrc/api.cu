@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 #include <stdarg.h>
 #include <math.h>
+#include <cmath>
 #include <algorithm>
 #include <nccl.h>
 
@@ -31,6 +32,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
 };
 static NcclApi g_nccl;
 
@@ -46,6 +49,8 @@ static bool nccl_load() {
   g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
   g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.CommGetAsyncError = (decltype(g_nccl.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+  g_nccl.CommCount = (decltype(g_nccl.CommCount))dlsym(h, "ncclCommCount");
   g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
   return g_nccl.loaded;
 }
@@ -78,7 +83,7 @@ void* scratch(Ctx* c, int slot, size_t bytes) {
   }
   size_t want = bytes + bytes / 4;
   static int dbg = -1;
-  if (dbg < 0) dbg = getenv("PPCA_DEBUG_SCRATCH") ? 1 : 0;
+  if (dbg < 0) dbg = tune_env("PPCA_DEBUG_SCRATCH", 0);
   if (dbg) fprintf(stderr, "[ppca] scratch slot %d grows to %zu bytes\n", slot, want);
   void* p = nullptr;
   if (cudaMalloc(&p, want) != cudaSuccess) {
@@ -106,14 +111,40 @@ ppca_status finish(Ctx* c, const char* what) {
   if (h & DEV_DEGENERATE) return set_error(c, PPCA_ERR_DEGENERATE, "%s: degenerate denominator / zero vector", what);
   if (h & DEV_COLLAPSE) return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "%s: orthonormalisation lost rank", what);
   if (h & DEV_NOCONV) return set_error(c, PPCA_ERR_NO_CONVERGENCE, "%s: Jacobi exceeded 100 sweeps", what);
+  if (h & DEV_TIMEOUT)
+    return set_error(c, PPCA_ERR_CUDA, "%s: an inter-CTA wait of the fused pass timed out (CTAs not co-resident)", what);
+  if (c->nccl_comm && g_nccl.CommGetAsyncError) {       // a communicator that failed asynchronously (peer lost, ...)
+    ncclResult_t ar = ncclSuccess;
+    if (g_nccl.CommGetAsyncError((ncclComm_t)c->nccl_comm, &ar) != ncclSuccess || ar != ncclSuccess)
+      return set_error(c, PPCA_ERR_NCCL, "%s: NCCL communicator error: %s", what, g_nccl.GetErrorString(ar));
+  }
   return PPCA_OK;
 }
 
+// In-place sum over the ranks on the context stream — the only collective of the path (BASELINE north_star:
+// "combined with NCCL allreduce").  A context without a communicator (world 1) skips it.
 ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64) {
-  if (c->world <= 1 || count == 0) return PPCA_OK;
+  if (!c->nccl_comm || count == 0) return PPCA_OK;
   ncclResult_t r = g_nccl.AllReduce(buf, buf, count, f64 ? ncclFloat64 : ncclFloat32, ncclSum,
                                     (ncclComm_t)c->nccl_comm, c->stream);
   if (r != ncclSuccess) return set_error(c, PPCA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+  c->collectives++;
+  return PPCA_OK;
+}
+
+// The per-iteration exchange [Z | S] (fp32 d×m and fp64 m×m) as ONE grouped NCCL operation (one launch,
+// one synchronisation point), SURVEY §8(e) "one fused buffer per step".
+ppca_status allreduce_zs(Ctx* c, float* Z, size_t nz, double* S, size_t ns) {
+  if (!c->nccl_comm) return PPCA_OK;
+  ncclResult_t r = g_nccl.GroupStart ? g_nccl.GroupStart() : ncclSuccess;
+  if (r == ncclSuccess && nz)
+    r = g_nccl.AllReduce(Z, Z, nz, ncclFloat32, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
+  if (r == ncclSuccess && ns)
+    r = g_nccl.AllReduce(S, S, ns, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
+  ncclResult_t r2 = g_nccl.GroupEnd ? g_nccl.GroupEnd() : ncclSuccess;
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return set_error(c, PPCA_ERR_NCCL, "grouped ncclAllReduce [Z|S]: %s", g_nccl.GetErrorString(r != ncclSuccess ? r : r2));
+  c->collectives++;
   return PPCA_OK;
 }
 
@@ -128,6 +159,25 @@ static ppca_status check_matrix(Ctx* c, const ppca_matrix* X, int m) {
   if (X->dtype == PPCA_F32_SPLIT && (X->d % 8 || (reinterpret_cast<uintptr_t>(X->data) % 16)))
     return set_error(c, PPCA_ERR_INVALID_ARG, "PPCA_F32_SPLIT needs d %% 8 == 0 and a 16-byte aligned X");
   if ((X->ld * (int64_t)elt_size(X->dtype)) % 16) return set_error(c, PPCA_ERR_INVALID_ARG, "ld*elt %% 16 != 0");
+  // the descriptor must describe exactly this rank's shard: kernels take row offsets from n_global
+  if (c->world == 1 && X->n_global != X->n_local)
+    return set_error(c, PPCA_ERR_DIM_MISMATCH, "one rank: n_global (%lld) must equal n_local (%lld)",
+                     (long long)X->n_global, (long long)X->n_local);
+  if (c->world > 1) {
+    int64_t want;
+    if (X->layout == PPCA_LAYOUT_INTERLEAVED) {
+      const int64_t b = X->block_rows;
+      if (b < 1 || b % c->world || (X->n_global % b) % c->world)
+        return set_error(c, PPCA_ERR_INVALID_ARG, "INTERLEAVED: world must divide block_rows and the last block");
+      want = (X->n_global / b) * (b / c->world) + (X->n_global % b) / c->world;
+    } else {
+      const int64_t per = ceil_div(X->n_global, (int64_t)c->world);
+      want = std::max<int64_t>(0, std::min<int64_t>(per, X->n_global - (int64_t)c->rank * per));
+    }
+    if (X->n_local != want)
+      return set_error(c, PPCA_ERR_DIM_MISMATCH, "rank %d: n_local = %lld, but the layout gives %lld rows", c->rank,
+                       (long long)X->n_local, (long long)want);
+  }
   if (m < 1) return set_error(c, PPCA_ERR_INVALID_ARG, "m must be >= 1");
   if (m > PPCA_MAX_M || m > X->d)
     return set_error(c, PPCA_ERR_TOO_MANY_COMPONENTS, "m=%d exceeds d=%lld or %d", m, (long long)X->d, PPCA_MAX_M);
@@ -209,14 +259,23 @@ ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank,
     delete h;
     return PPCA_ERR_CUDA;
   }
-  if (world > 1) {
-    if (!uid) { delete h; return PPCA_ERR_INVALID_ARG; }
+  // world > 1 needs the NCCL unique id; world == 1 with an id creates a one-rank communicator, so every
+  // collective call site of the path runs (and is tested) on a single GPU as well
+  if (world > 1 && !uid) { delete h; return PPCA_ERR_INVALID_ARG; }
+  if (uid) {
     if (!nccl_load()) { delete h; return PPCA_ERR_UNSUPPORTED; }
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
     ncclComm_t comm;
     if (g_nccl.CommInitRank(&comm, world, id, rank) != ncclSuccess) { delete h; return PPCA_ERR_NCCL; }
+    int cnt = 0;
+    if (g_nccl.CommCount && (g_nccl.CommCount(comm, &cnt) != ncclSuccess || cnt != world)) {
+      g_nccl.CommDestroy(comm);
+      delete h;
+      return PPCA_ERR_NCCL;
+    }
     c->nccl_comm = comm;
+    if (rank == 0 && world > 1) fprintf(stderr, "[ppca] NCCL communicator: %d ranks (rank 0 on device %d)\n", world, device);
   }
   *out = h;
   return PPCA_OK;
@@ -248,6 +307,15 @@ ppca_status ppca_last_error(const ppca_ctx* h, char* msg, size_t cap) {
 }
 
 int64_t ppca_launch_count(const ppca_ctx* h) { return h ? h->c.launches : -1; }
+int64_t ppca_collective_count(const ppca_ctx* h) { return h ? h->c.collectives : -1; }
+
+int ppca_experiments_enabled(void) {
+#ifdef PPCA_EXPERIMENTS
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 ppca_status ppca_set_timing(ppca_ctx* h, int enable) {
   if (!h) return PPCA_ERR_INVALID_ARG;
@@ -307,13 +375,15 @@ ppca_status ppca_philox_words(ppca_ctx* h, uint64_t seed, uint32_t stream, uint6
 }
 
 // ---------------------------------------------------------------------------- power priming
-ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters, uint64_t init_seed, float* W,
-                             double* theta_hist_host) {
+ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters, double eps, uint64_t init_seed,
+                             float* W, double* theta_hist_host, int* iters_done) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
   cudaSetDevice(c->device);
+  if (iters_done) *iters_done = 0;
   PPCA_TRY(check_matrix(c, X, m));
-  if (!W || iters < 0) return set_error(c, PPCA_ERR_INVALID_ARG, "null W or iters < 0");
+  if (!W || iters < 0 || !(eps == eps)) return set_error(c, PPCA_ERR_INVALID_ARG, "null W, iters < 0 or NaN eps");
+  const bool stop_rule = eps > 0.0;
   const int64_t d = X->d;
   if (init_seed) {
     PPCA_TRY(init_rows(c, init_seed, W, m, d));
@@ -324,6 +394,13 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   double* Sbuf = (double*)scratch(c, S_S, (size_t)4 * m * m * sizeof(double));      // S[2], Bm[2]
   double* theta_dev = (double*)scratch(c, S_TC2, (size_t)std::max(1, iters) * m * sizeof(double) + (size_t)m * m * sizeof(double));
   if (!Z || !Sbuf || !theta_dev) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  float* Wold = stop_rule ? (float*)scratch(c, S_EPS, (size_t)m * d * sizeof(float) + (size_t)m * sizeof(double)) : nullptr;
+  if (stop_rule && !Wold) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  double* dots = stop_rule ? reinterpret_cast<double*>(Wold + (size_t)m * d) : nullptr;
+  std::vector<double> hdots(stop_rule ? m : 0);
+  int done = 0;
+  if (theta_hist_host && iters > 0)
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(theta_dev, 0, (size_t)iters * m * sizeof(double), c->stream), "zero theta"));
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, m, &plan));
   // pre-touch the scratch the loop uses so no allocation happens while the side stream is busy
@@ -342,9 +419,8 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   }
   ppca_status st = PPCA_OK;
   c->side_busy = theta_hist_host != nullptr;
-  c->prep_ev = theta_hist_host ? ev_prep : nullptr;
   // one GPU with the θ history: S only feeds the side-stream Ritz solve, so its reduction moves there too
-  c->s_defer = theta_hist_host != nullptr && c->world == 1;
+  c->s_defer = theta_hist_host != nullptr && c->nccl_comm == nullptr;
   if (c->s_defer) {
     cudaEventCreateWithFlags(&c->s_ev_pass, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->s_ev_red, cudaEventDisableTiming);
@@ -353,21 +429,25 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   for (int t = 0; t < iters && st == PPCA_OK; ++t) {
     double* S = Sbuf + (size_t)(t & 1) * m * m;
     double* Bm = Sbuf + (size_t)(2 + (t & 1)) * m * m;
-    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);   // Ritz t-2 done with S, Bm
+    if (theta_hist_host) {
+      cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);   // Ritz t-2 done with S, Bm
+      cudaStreamWaitEvent(c->stream, ev_gram, 0);          // the side Gram of W'_{t-1} read it before prep_w rewrites
+    }
     st = pass_power(c, X, &plan, W, m, Z, S);               // Z = YᵀX, S = YᵀY  (local)
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
-      // side stream: Bm = W'W'ᵀ of the operand the pass uses (from ev_prep on, overlapping the pass), then
-      // the pPCA-for-free Ritz values of span(W'_t) once S_t is reduced
+      // side stream, once the pass is done (a Gram overlapping the persistent pass would take its SMs): Bm =
+      // W'W'ᵀ of the operand the pass used — concurrent with the main stream's CholQR — then the pPCA-for-free
+      // Ritz values of span(W'_t) once S_t is reduced
+      cudaEventRecord(ev_prep, c->stream);
       cudaStreamWaitEvent(c->side, ev_prep, 0);
       st = vec_gram_on(c, plan.Wop, m, d, Bm, c->side, S_SIDE_PART);
       if (st != PPCA_OK) break;
       cudaEventRecord(ev_gram, c->side);
-      st = pass_reduce_deferred_s(c, S, c->side);   // after the Gram: that one overlaps the pass
+      st = pass_reduce_deferred_s(c, S, c->side);
       if (st != PPCA_OK) break;
     }
-    st = allreduce(c, Z, (size_t)m * d, false);
-    if (st == PPCA_OK) st = allreduce(c, S, (size_t)m * m, true);
+    st = allreduce_zs(c, Z, (size_t)m * d, S, (size_t)m * m);   // the only collective: [Z | S], one group
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
       cudaEventRecord(ev_main[t & 1], c->stream);
@@ -377,9 +457,28 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       if (st != PPCA_OK) break;
     }
     // W ← orth(Z): one fp64 Cholesky-QR pass (κ(Z)² ε64 ≪ fp32 rounding for power iterates); it rewrites
-    // W (the SIMT pass's operand) and the next prep_w rewrites W' — after the side-stream Gram has read it
-    if (theta_hist_host) cudaStreamWaitEvent(c->stream, ev_gram, 0);
+    // W (the SIMT pass's operand: there the side Gram reads W itself, so wait for it) and the next prep_w
+    // rewrites W' (the wait at the top of the loop)
+    if (theta_hist_host && plan.impl != 2) cudaStreamWaitEvent(c->stream, ev_gram, 0);
+    if (stop_rule) {
+      st = check_cuda(c, cudaMemcpyAsync(Wold, W, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                      "keep W_t");
+      if (st != PPCA_OK) break;
+    }
     st = cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
+    if (st != PPCA_OK) break;
+    done = t + 1;
+    if (stop_rule) {                                 // P L61-62: stop once every column moved less than eps
+      st = row_dots(c, W, Wold, m, d, dots);
+      if (st == PPCA_OK)
+        st = check_cuda(c, cudaMemcpyAsync(hdots.data(), dots, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost,
+                                           c->stream), "stop rule");
+      if (st == PPCA_OK) st = check_cuda(c, cudaStreamSynchronize(c->stream), "stop rule");
+      if (st != PPCA_OK) break;
+      double worst = 0.0;                            // ‖w' − s·w‖² = 2 − 2|⟨w', w⟩| for unit columns
+      for (int j = 0; j < m; ++j) worst = std::max(worst, std::sqrt(std::max(0.0, 2.0 - 2.0 * std::fabs(hdots[j]))));
+      if (worst < eps) break;
+    }
   }
   c->prep_ev = nullptr;
   c->side_busy = false;
@@ -403,6 +502,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     if (cudaMemcpy(theta_hist_host, theta_dev, (size_t)iters * m * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
       return set_error(c, PPCA_ERR_CUDA, "copy theta");
   }
+  if (iters_done) *iters_done = done;
   return PPCA_OK;
 }
 
@@ -457,8 +557,7 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
       PPCA_TRY(ytx(c, X, r0, rows, Y, m, Q));
       PPCA_TRY(yty(c, Y, m, rows, P));
     }
-    PPCA_TRY(allreduce(c, Q, (size_t)m * d, false));
-    PPCA_TRY(allreduce(c, P, (size_t)m * m, true));
+    PPCA_TRY(allreduce_zs(c, Q, (size_t)m * d, P, (size_t)m * m));
     if (eigengame)
       PPCA_TRY(eigengame_update(c, Q, P, W, vel, m, d, alpha, mu));
     else
@@ -513,8 +612,10 @@ static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int
     const int64_t r0 = X->layout == PPCA_LAYOUT_CONTIGUOUS ? c->rank * ceil_div(X->n_global, (int64_t)c->world) : 0;
     rows_local = 0.0;
     for (int64_t t = 0; t < nt; ++t) {
-      const uint64_t key = X->layout == PPCA_LAYOUT_CONTIGUOUS ? (uint64_t)((r0 + t * tile) / tile)
-                                                               : ((uint64_t)c->rank << 40) + (uint64_t)t;
+      // key = the global index of the tile's first row (R25): distinct for every tile of every rank, so no two
+      // tiles share a draw; INTERLEAVED shards key on (rank, local tile) in a disjoint range
+      const uint64_t key = X->layout == PPCA_LAYOUT_CONTIGUOUS ? (uint64_t)(r0 + t * tile)
+                                                               : (1ull << 62) + ((uint64_t)c->rank << 40) + (uint64_t)t;
       if (u32_to_unit(philox_word(sample_seed, 7, key)) < fraction) {
         tiles.push_back((int32_t)t);
         rows_local += (double)(std::min(X->n_local, (t + 1) * tile) - t * tile);
@@ -522,7 +623,7 @@ static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int
     }
   }
   double rows_total = rows_local;
-  if (c->world > 1) {
+  if (c->nccl_comm) {
     double* cnt = S + 2 * (size_t)m * m;
     PPCA_TRY(check_cuda(c, cudaMemcpyAsync(cnt, &rows_local, sizeof(double), cudaMemcpyHostToDevice, c->stream), "count"));
     PPCA_TRY(allreduce(c, cnt, 1, true));
@@ -654,6 +755,36 @@ ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_
     while (s < k && ang[s] < thr_host[t]) ++s;
     lces_host[t] = s;
   }
+  return PPCA_OK;
+}
+
+// Certification support (reading R29): residual norms of Ritz pairs, one exact-fp32 SIMT
+// pass (Y = X·Eᵀ, Z = YᵀX with fp64 split-K sums; no bf16 rounding of E or Y), all-reduced.
+ppca_status ppca_ritz_residuals(ppca_ctx* h, const ppca_matrix* X, const float* E, int k, const double* theta_host,
+                                double* res_host) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  PPCA_TRY(check_matrix(c, X, k));
+  if (!E || !theta_host || !res_host) return set_error(c, PPCA_ERR_INVALID_ARG, "null E / theta / res");
+  const int64_t d = X->d;
+  float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, X->n_local) * k * sizeof(float));
+  float* Z = (float*)scratch(c, S_Z, (size_t)k * d * sizeof(float));
+  double* buf = (double*)scratch(c, S_EVAL, (size_t)2 * k * sizeof(double));
+  if (!Y || !Z || !buf) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (X->n_local > 0) {
+    PPCA_TRY(xw(c, X, 0, X->n_local, E, k, Y));
+    PPCA_TRY(ytx(c, X, 0, X->n_local, Y, k, Z));
+  } else {
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(Z, 0, (size_t)k * d * sizeof(float), c->stream), "zero Z"));
+  }
+  PPCA_TRY(allreduce(c, Z, (size_t)k * d, false));
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(buf, theta_host, (size_t)k * sizeof(double), cudaMemcpyHostToDevice,
+                                         c->stream), "copy theta"));
+  PPCA_TRY(ritz_resid(c, Z, E, buf, k, d, buf + k));
+  PPCA_TRY(finish(c, "ppca_ritz_residuals"));
+  if (cudaMemcpy(res_host, buf + k, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy residuals");
   return PPCA_OK;
 }
 

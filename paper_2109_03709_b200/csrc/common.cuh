@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,7 @@ enum DevErr : int {
   DEV_DEGENERATE = 2,
   DEV_COLLAPSE = 4,
   DEV_NOCONV = 8,
+  DEV_TIMEOUT = 16,     // a bounded inter-CTA wait expired (fused pass: CTAs not co-resident)
 };
 
 struct Ctx;
@@ -51,6 +53,7 @@ struct Ctx {
   int last_impl = 0;                  // implementation of the most recent pass
   int sm_count = 148;
   int64_t launches = 0;
+  int64_t collectives = 0;            // NCCL operations enqueued (bench evidence of the exchange)
   // pass timing (bench): event pairs recorded around each pass
   bool timing = false;
   std::vector<cudaEvent_t> tev;
@@ -85,6 +88,7 @@ enum Slot {
   S_NTSTAGE,
   S_P3,                            // Prop. 3 checker workspace (fp64)
   S_P3F,                           // Prop. 3 checker stacked vectors [B; T] (fp32)
+  S_EPS,                           // power stop rule: W_t copy + column dots
 };
 
 void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory
@@ -93,6 +97,7 @@ ppca_status set_error(Ctx* c, ppca_status s, const char* fmt, ...);
 ppca_status check_cuda(Ctx* c, cudaError_t e, const char* what);
 ppca_status finish(Ctx* c, const char* what);      // sync stream, read error word, map to status
 ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64);
+ppca_status allreduce_zs(Ctx* c, float* Z, size_t nz, double* S, size_t ns);   // grouped [Z | S]
 
 #define PPCA_TRY(expr)                         \
   do {                                         \
@@ -106,6 +111,28 @@ ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64);
     cudaError_t _e = cudaGetLastError();                                  \
     if (_e != cudaSuccess) return check_cuda((c), _e, what);              \
   } while (0)
+
+// Experiment switches (tuning sweeps, ablations, phase skips used while profiling): read from the
+// environment only in a build compiled with -DPPCA_EXPERIMENTS.  The shipped library always takes the
+// default, so no environment variable can change or skip its work (ppca_experiments_enabled() == 0).
+static inline int tune_env(const char* name, int dflt) {
+#ifdef PPCA_EXPERIMENTS
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
+// cudaFuncSetAttribute (dynamic shared memory opt-in) belongs to each device's context: call sites keep a
+// bit mask of the devices already configured and apply the attribute once per device.
+static inline bool first_on_device(uint64_t* mask, int dev) {
+  const uint64_t bit = 1ull << (dev & 63);
+  if (*mask & bit) return false;
+  *mask |= bit;
+  return true;
+}
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline size_t elt_size(ppca_dtype t) { return t == PPCA_BF16 ? 2 : 4; }

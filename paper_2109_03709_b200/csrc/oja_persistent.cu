@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(OJA_THREADS, 1) oja_persistent_kernel(OjaParam
 bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha, double mu, int64_t s0,
                     int64_t steps, float* W, float* vel, ppca_status* st) {
   *st = PPCA_OK;
-  if (c->world != 1 || m > OJA_MAXM || steps <= 0 || c->pass_impl != 0) return false;
+  if (c->world != 1 || c->nccl_comm || m > OJA_MAXM || steps <= 0 || c->pass_impl != 0) return false;
   const int64_t d = X->d;
   // short windows only (larger ones run the tensor-core window pass); one staged row must fit
   if ((int64_t)batch * d > ((int64_t)1 << 20) || d * (int64_t)sizeof(float) > OJA_XROW) return false;
@@ -474,10 +474,9 @@ bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha
     *st = set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
     return true;
   }
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(oja_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OJA_SMEM);
-    attr = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oja_persistent_kernel, OJA_THREADS, OJA_SMEM);
@@ -497,8 +496,8 @@ bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha
     p.wvec = ((uintptr_t)W % 16) == 0 && d % 4 == 0 ? 1 : 0;
   }
   p.clk = nullptr;
-  p.dbg = getenv("PPCA_OJA_DBG") ? atoi(getenv("PPCA_OJA_DBG")) : 0;
-  const bool want_clk = getenv("PPCA_OJA_CLK") != nullptr;
+  p.dbg = tune_env("PPCA_OJA_DBG", 0);
+  const bool want_clk = tune_env("PPCA_OJA_CLK", 0) != 0;
   if (want_clk) p.clk = (unsigned long long*)(Q + (size_t)m * d);
   void* args[] = {&p};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)oja_persistent_kernel, grid, OJA_THREADS, args, OJA_SMEM,

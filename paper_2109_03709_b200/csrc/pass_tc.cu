@@ -87,17 +87,24 @@ __device__ __forceinline__ float4 ldg_x4(const float* __restrict__ X, int64_t ld
 // span the tensor cores see is W to ~2^-17 (a single bf16 W would move a non-invariant span by ~2^-9
 // and its Ritz values at first order).  Wr = hi + lo (fp32) is the operand's exact value, used for the
 // Rayleigh–Ritz Gram and the lift.
+// four consecutive elements per thread (d % 8 == 0 on the tensor-core path): 16-byte loads / stores
 __global__ void prep_w_kernel(const float* __restrict__ W, int m, int mp, int64_t d, __nv_bfloat16* __restrict__ Wb,
                               float* __restrict__ Wr) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e >= (int64_t)mp * d) return;
-  int64_t i = e / d;
-  float v = i < m ? W[e] : 0.f;
-  __nv_bfloat16 hi = __float2bfloat16_rn(v);
-  __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-  Wb[e] = hi;
-  Wb[e + (int64_t)mp * d] = lo;
-  if (i < m) Wr[e] = __bfloat162float(hi) + __bfloat162float(lo);
+  const int64_t i = e / d;
+  const float4 v = i < m ? __ldg(reinterpret_cast<const float4*>(W + e)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint2 hi = pack4_bf16(v);
+  const uint2 lo = pack4_bf16(residual_bf16(v, hi));
+  *reinterpret_cast<uint2*>(Wb + e) = hi;
+  *reinterpret_cast<uint2*>(Wb + e + (int64_t)mp * d) = lo;
+  if (i < m) {
+    *reinterpret_cast<float4*>(Wr + e) =
+        make_float4(__uint_as_float(hi.x << 16) + __uint_as_float(lo.x << 16),
+                    __uint_as_float(hi.x & 0xffff0000u) + __uint_as_float(lo.x & 0xffff0000u),
+                    __uint_as_float(hi.y << 16) + __uint_as_float(lo.y << 16),
+                    __uint_as_float(hi.y & 0xffff0000u) + __uint_as_float(lo.y & 0xffff0000u));
+  }
 }
 
 // ============================================================================ kernel A (tc_xw.cuh)
@@ -362,7 +369,7 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
   if (!buf) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   *Wb = reinterpret_cast<__nv_bfloat16*>(buf);
   *Wr = reinterpret_cast<float*>(buf + (((size_t)2 * mp * d * 2 + 255) & ~(size_t)255));
-  prep_w_kernel<<<(unsigned)ceil_div((int64_t)mp * d, 256), 256, 0, c->stream>>>(W, m, mp, d, *Wb, *Wr);
+  prep_w_kernel<<<(unsigned)ceil_div((int64_t)mp * d, 1024), 256, 0, c->stream>>>(W, m, mp, d, *Wb, *Wr);
   PPCA_LAUNCH_CHECK(c, "prep_w");
   return PPCA_OK;
 }
@@ -373,7 +380,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   // kernel A2 on CTA pairs (2-CTA UMMA, W' split across the pair): bf16 X with m padded to 128 (C5), whole
   // tiles; PPCA_A2_PAIR=0 disables
   static int pair_env = -1;
-  if (pair_env < 0) pair_env = getenv("PPCA_A2_PAIR") ? atoi(getenv("PPCA_A2_PAIR")) : 1;
+  if (pair_env < 0) pair_env = tune_env("PPCA_A2_PAIR", 1);
   const bool pair = pair_env && X->dtype == PPCA_BF16 && mp == 128 && ksplit == 1 && tiles == nullptr &&
                     persistent_ctas(c) >= 2;
   CUtensorMap tmW, tmX, tmXlo;
@@ -391,7 +398,7 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   kp.kper = ceil_div(kp.nk, (int64_t)ksplit);
   kp.Ypart = Ypart;
   static int dbg = -1;
-  if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
+  if (dbg < 0) dbg = tune_env("PPCA_DBG", 0);
   kp.dbg = dbg;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit));
   if (pair) grid = (int)std::max<int64_t>(2, std::min<int64_t>(persistent_ctas(c) & ~1, 2 * ((kp.ntiles + 1) / 2)));
@@ -521,27 +528,47 @@ static constexpr size_t fused_smem() {
          (size_t)NSTB * (kf::BX + kf::BY) + 256;
 }
 
+// The CTAs of a row group wait on each other's tile flags, so the grid must be co-resident: a cooperative
+// launch guarantees it or fails (cudaErrorCooperativeLaunchTooLarge: fewer free SMs than CTAs, e.g. under an
+// MPS / green-context partition), in which case the caller runs the two-kernel pass instead.
 template <int XM, int NSTA, int NWS, int NSTB>
-static void launch_fused(Ctx* c, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
-                         const CUtensorMap& tmXb, const CUtensorMap& tmY, const KFParams& fp) {
+static cudaError_t launch_fused(Ctx* c, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                                const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const CUtensorMap& tmY,
+                                const KFParams& fp) {
   constexpr size_t smem = fused_smem<XM, NSTA, NWS, NSTB>();
   static_assert(smem <= 227 * 1024, "fused kernel shared memory budget");
   auto kern = xwz_fused_kernel<XM, NSTA, NWS, NSTB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kf::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, tmXb, tmY, fp);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kf::NTHREADS, smem) != cudaSuccess ||
+      per_sm * c->sm_count < grid) {
+    cudaGetLastError();
+    return cudaErrorCooperativeLaunchTooLarge;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kf::NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmXlo, tmXb, tmY, fp);
 }
 
 template <int XM>
-static void launch_fused_cfg(Ctx* c, int cfg, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
-                             const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const CUtensorMap& tmY,
-                             const KFParams& fp) {
+static cudaError_t launch_fused_cfg(Ctx* c, int cfg, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                                    const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const CUtensorMap& tmY,
+                                    const KFParams& fp) {
   // (X stages, W' stages, B stages of KR = 64 rows).  Measured on C3, one box: 32-row B stages (2,2,5)
   // 1.088 ms -> 64-row B stages (2,2,2) 0.951 ms, (3,2,2) 0.993, (2,1,3) 1.018 (larger TMA boxes and half
-  // the B-stream barrier round trips); PPCA_FUSED_CFG selects the others
+  // the B-stream barrier round trips); PPCA_FUSED_CFG (experiment builds) selects the others
   switch (cfg) {
-    case 6: launch_fused<XM, 3, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    case 7: launch_fused<XM, 2, 1, 3>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
-    default: launch_fused<XM, 2, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp); break;
+    case 6: return launch_fused<XM, 3, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+    case 7: return launch_fused<XM, 2, 1, 3>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+    default: return launch_fused<XM, 2, 2, 2>(c, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
   }
 }
 
@@ -552,8 +579,10 @@ static bool fused_eligible(const Ctx* c, const ppca_matrix* X, int mp, bool prec
          X->n_local >= 128;
 }
 
+// *launched = false (status OK) when the grid cannot be co-resident: the caller runs the two-kernel pass.
 static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, float* Z,
-                                    double* S) {
+                                    double* S, bool* launched) {
+  *launched = false;
   const int mp = 64;
   const int64_t n = X->n_local, d = X->d;
   const int64_t ntiles = ceil_div(n, kf::BM);
@@ -601,29 +630,35 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   fp.Yrm = Yrm; fp.nrow_pad = nrow_pad; fp.Spart = Spart; fp.Zp = Zp;
   fp.flags = c->flags; fp.epoch = c->epoch;
   static int pf = -1;
-  if (pf < 0) pf = getenv("PPCA_FUSED_PF") ? atoi(getenv("PPCA_FUSED_PF")) : 0;
+  if (pf < 0) pf = tune_env("PPCA_FUSED_PF", 0);
   fp.pf = pf;
   static int dbg = -1;
-  if (dbg < 0) dbg = getenv("PPCA_DBG") ? atoi(getenv("PPCA_DBG")) : 0;
+  if (dbg < 0) dbg = tune_env("PPCA_DBG", 0);
   fp.dbg = dbg;
   static int hip = -1;
-  if (hip < 0) hip = getenv("PPCA_FUSED_HI") ? atoi(getenv("PPCA_FUSED_HI")) : 0;
+  if (hip < 0) hip = tune_env("PPCA_FUSED_HI", 0);
   fp.hi_policy = hip;
   static int lag = -1;
   // A-stream lead over the B-stream capped at 2 rounds (measured on C3: dram reads 5.73 → 5.41 GB, pass
   // −1.6 %; 1 round starves the overlap, 3 = unbounded); PPCA_FUSED_LAG overrides (0 = off)
-  if (lag < 0) lag = getenv("PPCA_FUSED_LAG") ? atoi(getenv("PPCA_FUSED_LAG")) : 2;
+  if (lag < 0) lag = tune_env("PPCA_FUSED_LAG", 2);
   fp.lag = lag;
+  fp.err = c->d_err;
   if (c->s_defer) cudaStreamWaitEvent(c->stream, c->s_ev_red, 0);   // the previous S partials were reduced
   kernel_timer_mark(c, 0);
   static int cfg = -1;
-  if (cfg < 0) cfg = getenv("PPCA_FUSED_CFG") ? atoi(getenv("PPCA_FUSED_CFG")) : 0;
-  if (X->dtype == PPCA_F32_SPLIT)
-    launch_fused_cfg<2>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
-  else
-    launch_fused_cfg<1>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+  if (cfg < 0) cfg = tune_env("PPCA_FUSED_CFG", 0);
+  const cudaError_t le = X->dtype == PPCA_F32_SPLIT ? launch_fused_cfg<2>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp)
+                                                    : launch_fused_cfg<1>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, tmY, fp);
+  if (le == cudaErrorCooperativeLaunchTooLarge) {   // not co-resident here: nothing was launched
+    cudaGetLastError();
+    if (c->timing && c->kev_used[0] > 0) c->kev_used[0]--;   // drop the unmatched timer mark
+    return PPCA_OK;
+  }
+  if (le != cudaSuccess) return check_cuda(c, le, "xwz_fused_kernel");
   PPCA_LAUNCH_CHECK(c, "xwz_fused_kernel");
   kernel_timer_mark(c, 0);
+  *launched = true;
   if (c->s_defer) {                               // S is reduced later, on the stream that consumes it
     cudaEventRecord(c->s_ev_pass, c->stream);
     c->s_pending = true;
@@ -657,13 +692,22 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   const int64_t n = X->n_local, d = X->d;
   __nv_bfloat16* Wb;
   float* Wr;
+  // reading R30: product 2 of a power pass reads X_hi alone, an error that averages down over the rows
+  // (2.9e-5 on the Ritz values at n = 10^5 against the 1e-4 bar, ~1e-4 at n = 2000); below kPreciseRows global
+  // rows of a split X the pass adds X_lo·Y_hi (kernel B's XLO instantiation) — the cost is nil at that size
+  constexpr int64_t kPreciseRows = 32768;
+  precise = precise || (X->dtype == PPCA_F32_SPLIT && X->n_global < kPreciseRows);
   const bool fused = fused_eligible(c, X, mp, precise);
   // bf16 X outside the fused kernel and outside the minibatch steps: product 2 with Y_hi alone (R27)
   const bool lean = X->dtype == PPCA_BF16 && !fused && !precise;
   PPCA_TRY(prep_w(c, W, m, mp, d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
   if (c->prep_ev) cudaEventRecord(c->prep_ev, c->stream);     // W' ready: the side stream may read Wr
-  if (fused) return pass_fused_power(c, X, Wb, m, Z, S);
+  if (fused) {
+    bool launched = false;
+    PPCA_TRY(pass_fused_power(c, X, Wb, m, Z, S, &launched));
+    if (launched) return PPCA_OK;
+  }
   // Yᵀ as a bf16 pair [Y_hi; Y_lo], [2·mp][ldyt]; kernel A writes every row and column < ldyt
   const int64_t ldyt = ceil_div(n, 64) * 64;
   __nv_bfloat16* YT = (__nv_bfloat16*)scratch(c, S_Y, (size_t)2 * mp * ldyt * 2);

@@ -7,8 +7,94 @@
 namespace ppca {
 
 // ============================================================================ vector Gram
+// G_ij = Σ_x V[i][x] V[j][x] (fp64), the CholQR / operand Gram of the m×m chain (d·m² MAC).
+// fp64 FMA throughput bound (64 DFMA / clk / SM): each CTA takes a d-slab, stages GK columns of all m rows
+// as fp64 in shared memory ([column][row], so a thread's 8 row values are two 16-byte loads), and every thread
+// accumulates one 8×8 register tile of the upper triangle (8 + 8 operand loads per 64 DFMA, warp-broadcast).
+// The next stage's fp32 values are loaded into registers while the current one is consumed.  Partials hold
+// both triangles of the slab's Gram; launch_reduce_splits_f64 sums the slabs in a fixed order.
+constexpr int GK = 32;                            // columns per stage
+constexpr int GRAM_MAXT = 160;                    // threads for m ≤ 128: 136 upper 8×8 tiles
+
+template <int MB>                                 // MB = ceil(m / 8) (≤ 16)
+__global__ void __launch_bounds__(GRAM_MAXT) vec_gram_tiled_kernel(const float* __restrict__ V, int m, int64_t d,
+                                                                   int64_t cols_per_split, double* __restrict__ P) {
+  constexpr int MP = MB * 8, LD = MP + 2;         // +2 doubles: 16-byte aligned rows, 4-way worst transposed store
+  constexpr int NT = MB * (MB + 1) / 2;           // upper tiles
+  constexpr int PER = (MP * GK + GRAM_MAXT - 1) / GRAM_MAXT;
+  __shared__ __align__(16) double sv[GK * LD];
+  const int64_t xb = (int64_t)blockIdx.x * cols_per_split;
+  const int64_t xe = min(d, xb + cols_per_split);
+  // tile (bi ≤ bj) of this thread
+  int bi = 0, bj = 0;
+  {
+    int t = threadIdx.x, row = 0;
+    while (row < MB && t >= MB - row) { t -= MB - row; ++row; }
+    bi = row;
+    bj = row + t;
+  }
+  const bool active = threadIdx.x < NT;
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  float nxt[PER];
+  auto fetch = [&](int64_t x0) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + GRAM_MAXT * u;  // e = row·GK + column: a warp reads 32 consecutive columns
+      const int r = e / GK, cc = e % GK;
+      const int64_t x = x0 + cc;
+      nxt[u] = (e < MP * GK && r < m && x < xe) ? __ldg(V + (int64_t)r * d + x) : 0.f;
+    }
+  };
+  if (xb < xe) fetch(xb);
+  for (int64_t x0 = xb; x0 < xe; x0 += GK) {
+    __syncthreads();                               // the previous stage is consumed
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + GRAM_MAXT * u;
+      if (e < MP * GK) sv[(e % GK) * LD + e / GK] = (double)nxt[u];
+    }
+    __syncthreads();
+    if (x0 + GK < xe) fetch(x0 + GK);              // in flight while this stage is consumed
+    if (active) {
+#pragma unroll 4
+      for (int k = 0; k < GK; ++k) {
+        const double2* pa = reinterpret_cast<const double2*>(sv + k * LD + bi * 8);
+        const double2* pb = reinterpret_cast<const double2*>(sv + k * LD + bj * 8);
+        double a[8], b[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 va = pa[q], vb = pb[q];
+          a[2 * q] = va.x; a[2 * q + 1] = va.y;
+          b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+    }
+  }
+  if (!active) return;
+  double* Pz = P + (int64_t)blockIdx.x * m * m;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gi = bi * 8 + i, gj = bj * 8 + j;
+      if (gi < m && gj < m) {
+        Pz[(int64_t)gi * m + gj] = acc[i][j];
+        Pz[(int64_t)gj * m + gi] = acc[i][j];      // both triangles (diagonal tiles write the same values twice)
+      }
+    }
+}
+
+// generic 32×32-tile Gram (m > 128: the Prop. 3 checker's stacked [B; T] Gram)
 // G_ij = Σ_x V[i][x] V[j][x]; tile 32×32 outputs × 64-column chunks, split over d.
-__global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__ V, int m, int64_t d,
+__global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __restrict__ V, int m, int64_t d,
                                                        int64_t cols_per_split, double* __restrict__ P) {
   __shared__ float Vi[32][65];
   __shared__ float Vj[32][65];
@@ -53,11 +139,10 @@ __global__ void __launch_bounds__(256) vec_gram_kernel(const float* __restrict__
 }
 
 static void vec_gram_split(const Ctx* c, int m, int64_t d, int* nsplit_out, int64_t* cps_out) {
-  const int tiles = (int)ceil_div(m, 32);
-  const int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
-  const int64_t maxs = ceil_div(d, 64);
-  int nsplit = (int)std::max<int64_t>(1, std::min(want, maxs));
-  const int64_t cps = ceil_div(ceil_div(d, nsplit), 64) * 64;
+  (void)m;
+  const int64_t stages = ceil_div(d, (int64_t)GK);
+  const int64_t want = std::min<int64_t>(stages, (int64_t)c->sm_count);
+  const int64_t cps = ceil_div(stages, want) * GK;
   *nsplit_out = (int)ceil_div(d, cps);
   *cps_out = cps;
 }
@@ -69,14 +154,29 @@ size_t vec_gram_part_bytes(const Ctx* c, int m, int64_t d) {
   return (size_t)ns * m * m * sizeof(double);
 }
 
+template <int MB>
+static void launch_gram_mb(int nsplit, cudaStream_t st, const float* V, int m, int64_t d, int64_t cps, double* P) {
+  vec_gram_tiled_kernel<MB><<<nsplit, GRAM_MAXT, 0, st>>>(V, m, d, cps, P);
+}
+
 ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cudaStream_t st, int part_slot) {
-  const int tiles = (int)ceil_div(m, 32);
   int nsplit;
   int64_t cps;
   vec_gram_split(c, m, d, &nsplit, &cps);
   double* P = (double*)scratch(c, part_slot, (size_t)nsplit * m * m * sizeof(double));
   if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  vec_gram_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
+  const int mb = (int)ceil_div(m, 8);
+  if (mb <= 1) launch_gram_mb<1>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 2) launch_gram_mb<2>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 4) launch_gram_mb<4>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 6) launch_gram_mb<6>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 8) launch_gram_mb<8>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 12) launch_gram_mb<12>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 16) launch_gram_mb<16>(nsplit, st, V, m, d, cps, P);
+  else {
+    const int tiles = (int)ceil_div(m, 32);
+    vec_gram_generic_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
+  }
   PPCA_LAUNCH_CHECK(c, "vec_gram");
   return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G, st);
 }
@@ -260,7 +360,7 @@ __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop
 // double-buffered shared memory — one barrier per step, no index arithmetic in the loop (the blocked
 // shared-memory version's cost, tools/microbench_small.cu).  Rows/columns ≥ m are the identity.
 constexpr int CF_M = 64;
-static const bool g_chol_reg = !(getenv("PPCA_CHOL_REG") && atoi(getenv("PPCA_CHOL_REG")) == 0);
+static const bool g_chol_reg = tune_env("PPCA_CHOL_REG", 1) != 0;
 // the sweep as a block-level device function (blockDim.x == 64·CQ): G [m][m] and Linv [m][ldl] in any
 // memory space; keep[i] = 1 (no drops); a non-positive pivot flags DEV_COLLAPSE.  Used by the CholQR kernel
 // below and by the Ritz kernels (ritz.cuh) for the operand Gram's L⁻¹.
@@ -336,7 +436,7 @@ __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __r
   if (threadIdx.x == 0) *m_out = m;
 }
 
-static int g_chol_cq = getenv("PPCA_CHOL_CQ") ? atoi(getenv("PPCA_CHOL_CQ")) : 8;
+static int g_chol_cq = tune_env("PPCA_CHOL_CQ", 8);
 static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_map, int* m_out, int* d_err,
                                 cudaStream_t st) {
   if (g_chol_cq == 4)
@@ -358,73 +458,123 @@ static size_t chol_inv_smem(int m) {
 // rows × m_in block of C (fp64) and the m_in × 32 slab of IN are staged in shared memory with every load
 // in flight at once (the inner loop then never waits on L2), warp w computes rows i ≡ w (mod 8) with
 // lane = column (C[i][j] a shared-memory broadcast).
-constexpr int AP_COLS = 32;
-__global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
-                                                         int m_in, const int* __restrict__ row_map,
-                                                         bool lower, const float* __restrict__ IN,
-                                                         int64_t d, float* __restrict__ OUT, int rows_per_cta) {
-  extern __shared__ double cs[];                 // this CTA's rows × m_in (fp64), then m_in × AP_COLS (fp32)
-  const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
-  float* ins = reinterpret_cast<float*>(cs + (size_t)rows_per_cta * m_in);
-  const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
-  copy_batched<16>(threadIdx.x, (r1 - r0) * m_in, blockDim.x,
-                   [&](int64_t e) { return C[(r0 + e / m_in) * ldc + e % m_in]; },
-                   [&](int64_t e, double v) { cs[e] = v; });
-  copy_batched<8>(threadIdx.x, m_in * AP_COLS, blockDim.x,
+// OUT[row_map(i)] = Σ_j C[i][j]·IN[j] for i < rows (C fp64 [rows][ldc], IN [m_in][d] fp32, fp64 accumulation;
+// lower: C lower-triangular).  The apply of CholQR (W = L⁻¹Z, d·m²/2 MAC), the lift E = R·B and the EigenGame
+// mixing.  fp64-FMA bound: a grid of ≤ one CTA per SM, each holding Cᵀ in shared memory once and sweeping
+// 32-column chunks of IN; thread = RPT rows × 4 columns of the output chunk (RPT + 4 operand loads per 4·RPT
+// DFMA, warp-broadcast), the next chunk's IN loaded into registers while the current one is consumed.
+constexpr int AT_COLS = 32;
+
+template <int RPT>
+__global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restrict__ C, int ldc, int rows, int m_in,
+                                                          const int* __restrict__ row_map, bool lower,
+                                                          const float* __restrict__ IN, int64_t d,
+                                                          float* __restrict__ OUT) {
+  constexpr int RP = 32 * RPT, LDT = RP + 2;      // Cᵀ rows padded: 16-byte aligned, 4-way worst transposed store
+  constexpr int PER = (128 * AT_COLS) / 256;      // staged IN values per thread (m_in ≤ 128)
+  extern __shared__ __align__(16) double ct[];    // [m_in][LDT] fp64, then [m_in][AT_COLS] fp32
+  float* ins = reinterpret_cast<float*>(ct + (size_t)m_in * LDT);
+  copy_batched<8>(threadIdx.x, (int64_t)rows * m_in, 256,
                   [&](int64_t e) {
-                    const int64_t x = x0 + e % AP_COLS;
-                    return IN[(e / AP_COLS) * d + (x < d ? x : d - 1)];
+                    const int i = (int)(e / m_in), j = (int)(e % m_in);
+                    return (!lower || j <= i) ? C[(int64_t)i * ldc + j] : 0.0;
                   },
-                  [&](int64_t e, float v) { ins[e] = x0 + e % AP_COLS < d ? v : 0.f; });
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t x = x0 + lane;
-  for (int i = r0 + warp; i < r1; i += 8) {
-    const int oi = row_map ? row_map[i] : i;
-    if (oi < 0) continue;
-    const double* crow = cs + (size_t)(i - r0) * m_in;
-    const int jend = lower ? min(i + 1, m_in) : m_in;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: the FMA latency is hidden
-    int j = 0;
-    for (; j + 4 <= jend; j += 4) {
-      a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
-      a1 = fma(crow[j + 1], (double)ins[(j + 1) * AP_COLS + lane], a1);
-      a2 = fma(crow[j + 2], (double)ins[(j + 2) * AP_COLS + lane], a2);
-      a3 = fma(crow[j + 3], (double)ins[(j + 3) * AP_COLS + lane], a3);
+                  [&](int64_t e, double v) { ct[(e % m_in) * LDT + e / m_in] = v; });
+  for (int e = threadIdx.x; e < m_in * (RP - rows); e += 256) ct[(e / (RP - rows)) * LDT + rows + e % (RP - rows)] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = lane >> 3, cg = lane & 7;
+  const int i0 = warp * 4 * RPT + rg * RPT;
+  const int jend = lower ? min(m_in, (warp + 1) * 4 * RPT) : m_in;    // warp-uniform
+  const int64_t nchunks = (d + AT_COLS - 1) / AT_COLS;
+  float nxt[PER];
+  auto fetch = [&](int64_t ch) {
+    const int64_t x0 = ch * AT_COLS;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u, j = e / AT_COLS;
+      const int64_t x = x0 + e % AT_COLS;
+      nxt[u] = (j < m_in && x < d) ? __ldg(IN + (int64_t)j * d + x) : 0.f;
     }
-    for (; j < jend; ++j) a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
-    if (x < d) OUT[(int64_t)oi * d + x] = (float)((a0 + a1) + (a2 + a3));
+  };
+  int64_t ch = blockIdx.x;
+  if (ch < nchunks) fetch(ch);
+  for (; ch < nchunks; ch += gridDim.x) {
+    __syncthreads();                               // Cᵀ written / the previous chunk consumed
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      if (e < m_in * AT_COLS) ins[e] = nxt[u];
+    }
+    __syncthreads();
+    if (ch + gridDim.x < nchunks) fetch(ch + gridDim.x);
+    double acc[RPT][4];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < jend; ++j) {
+      const float4 b = *reinterpret_cast<const float4*>(ins + j * AT_COLS + cg * 4);
+      double a[RPT];
+      if constexpr (RPT == 1) {
+        a[0] = ct[j * LDT + i0];
+      } else {
+#pragma unroll
+        for (int r = 0; r < RPT; r += 2) {        // i0 is even for RPT ≥ 2: 16-byte aligned pairs
+          const double2 v = *reinterpret_cast<const double2*>(ct + j * LDT + i0 + r);
+          a[r] = v.x;
+          a[r + 1] = v.y;
+        }
+      }
+      const double bb[4] = {(double)b.x, (double)b.y, (double)b.z, (double)b.w};
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q] = fma(a[r], bb[q], acc[r][q]);
+    }
+    const int64_t x0 = ch * AT_COLS + cg * 4;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = i0 + r;
+      if (i >= rows) continue;
+      const int oi = row_map ? row_map[i] : i;
+      if (oi < 0) continue;
+      float* o = OUT + (int64_t)oi * d;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (x0 + q < d) o[x0 + q] = (float)acc[r][q];
+    }
   }
+}
+
+template <int RPT>
+static void launch_apply_tiled(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map, bool lower,
+                               const float* IN, int64_t d, float* OUT, cudaStream_t st) {
+  const size_t smem = (size_t)m_in * (32 * RPT + 2) * sizeof(double) + (size_t)m_in * AT_COLS * sizeof(float);
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device))
+    cudaFuncSetAttribute(apply_tiled_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int64_t nchunks = ceil_div(d, (int64_t)AT_COLS);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nchunks, c->sm_count));
+  apply_tiled_kernel<RPT><<<grid, 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
 }
 
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
                               bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  // row blocks (multiples of 8 rows) until the grid covers the SMs: d = 1024 alone gives 32 CTAs
-  const int64_t gx = ceil_div(d, (int64_t)AP_COLS);
-  static const bool split = !(getenv("PPCA_APPLY_SPLIT") && atoi(getenv("PPCA_APPLY_SPLIT")) == 0);
-  int rpc = rows;
-  if (split && gx < c->sm_count) {
-    const int gy = (int)std::min<int64_t>(ceil_div((int64_t)c->sm_count, gx), ceil_div((int64_t)rows, (int64_t)8));
-    rpc = (int)ceil_div((int64_t)ceil_div((int64_t)rows, (int64_t)gy), (int64_t)8) * 8;
-  }
-  const unsigned gy = (unsigned)ceil_div((int64_t)rows, (int64_t)rpc);
-  size_t smem = (size_t)rpc * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
-  apply_rows_kernel<<<dim3((unsigned)gx, gy), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
+  if (rows < 1 || m_in < 1 || d < 1) return PPCA_OK;
+  if (rows > 128 || m_in > 128) return set_error(c, PPCA_ERR_UNSUPPORTED, "apply: %d x %d > 128", rows, m_in);
+  if (rows <= 32) launch_apply_tiled<1>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
+  else if (rows <= 64) launch_apply_tiled<2>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
+  else launch_apply_tiled<4>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
 
 // L⁻¹ of chol(G) (one CTA, fp64) on stream st; no drops (a non-positive pivot flags DEV_COLLAPSE)
 ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_map, int* m_out, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   if (m <= CF_M && g_chol_reg) {
     launch_chol_inv_reg(G, m, Linv, row_map, m_out, c->d_err, st);
@@ -456,10 +606,9 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   int* d_mout = row_map + m;
   float* T = (float*)scratch(c, S_W2, (size_t)m * d * sizeof(float));
   if (!G || !Linv || !T) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   const size_t smem = chol_inv_smem(m);
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
@@ -519,19 +668,17 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
                        cudaStream_t stream) {
   double* scr = (double*)scratch(c, S_EVAL, (size_t)2 * m * m * sizeof(double));
   if (!scr) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(ritz::ritz_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
     cudaFuncSetAttribute(ritz::ritz_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
-    attr = true;
   }
   static int jacobi = -1;                         // PPCA_RITZ_JACOBI=1: the Jacobi solver for vectors too
-  if (jacobi < 0) jacobi = getenv("PPCA_RITZ_JACOBI") ? atoi(getenv("PPCA_RITZ_JACOBI")) : 0;
+  if (jacobi < 0) jacobi = tune_env("PPCA_RITZ_JACOBI", 0);
   if (!R_dev || (m <= 64 && !jacobi)) {           // tridiagonalisation + multisection (+ inverse iteration)
-    static bool vattr = false;
-    if (!vattr) {
+    static uint64_t vattr = 0;
+    if (first_on_device(&vattr, c->device)) {
       cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      vattr = true;
     }
     ritz::ritz_values_kernel<<<1, 512, ritz::values_smem_bytes(m), stream>>>(S, Bm, m, scr, scr + (size_t)m * m,
                                                                               theta_dev, c->d_err, R_dev);
@@ -885,10 +1032,9 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
   const int64_t nchunks = ceil_div(d, (int64_t)EG_XC);
   const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) +
                       std::max((size_t)m * EG_XC * sizeof(float), (size_t)256 * sizeof(double));
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(eg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   int per_sm = 0;
   if (smem > 200 * 1024 ||
@@ -917,7 +1063,7 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
 ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
                              double alpha, double mu) {
   static int multi = -1;                          // PPCA_EG_MULTI=1: the 5-launch sequence (comparison)
-  if (multi < 0) multi = getenv("PPCA_EG_MULTI") ? atoi(getenv("PPCA_EG_MULTI")) : 0;
+  if (multi < 0) multi = tune_env("PPCA_EG_MULTI", 0);
   if (!multi) {
     ppca_status st;
     if (eigengame_update_fused(c, MV, A, V, vel, m, d, alpha, mu, &st)) return st;
@@ -951,6 +1097,34 @@ __global__ void row_dots_kernel(const float* __restrict__ E, const float* __rest
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
     out[blockIdx.x] = t;
   }
+}
+
+// res[i] = ‖Z_i − θ_i E_i‖ in fp64 (Z_i = (XᵀX e_i)ᵀ), one CTA per vector
+__global__ void ritz_resid_kernel(const float* __restrict__ Z, const float* __restrict__ E,
+                                  const double* __restrict__ theta, int64_t d, double* __restrict__ out) {
+  const float* z = Z + (int64_t)blockIdx.x * d;
+  const float* e = E + (int64_t)blockIdx.x * d;
+  const double th = theta[blockIdx.x];
+  double s = 0.0;
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
+    const double r = (double)z[x] - th * (double)e[x];
+    s = fma(r, r, s);
+  }
+  s = warp_sum(s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[blockIdx.x] = sqrt(t);
+  }
+}
+
+ppca_status ritz_resid(Ctx* c, const float* Z, const float* E, const double* theta, int k, int64_t d, double* res) {
+  ritz_resid_kernel<<<k, 256, 0, c->stream>>>(Z, E, theta, d, res);
+  PPCA_LAUNCH_CHECK(c, "ritz_resid");
+  return PPCA_OK;
 }
 
 ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots) {

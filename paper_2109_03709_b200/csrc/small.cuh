@@ -56,5 +56,7 @@ ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V,
 ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm, int upto, double* ratio_host,
                          double* angles_host);
 ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots);
+// res[i] = ‖Z_i − θ_i E_i‖ (fp64), θ device double[k]
+ppca_status ritz_resid(Ctx* c, const float* Z, const float* E, const double* theta, int k, int64_t d, double* res);
 
 }  // namespace ppca

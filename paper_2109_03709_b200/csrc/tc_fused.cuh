@@ -9,7 +9,8 @@
 // group then accumulates product 2 for its own d-group over ALL the group's tiles ("B-work": waits for the
 // tile's flag, TMA-loads Yᵀ and X_hi[tile, d-group] — which a sibling has just pulled through L2).
 // Rounds keep the siblings in step: round ρ = the ndg tiles ρ·ndg + j; A-work of round ρ precedes B-work of
-// round ρ in every CTA.  All CTAs are co-resident (persistent, ≤ one per SM), so the flag waits terminate.
+// round ρ in every CTA.  All CTAs are co-resident (cooperative launch, ≤ one per SM), so the flag waits
+// terminate; each wait is also bounded (kFlagTimeoutNs → DEV_TIMEOUT).
 //
 // TMEM (512 columns): Y accumulator [0, 128) (one buffer), S [128, 256), Zᵀ [256, 512) (two 128-row d-chunks
 // × N = 128 = [Y_hi; Y_lo]).  Shared memory (default configuration): A ring 2 × 32 KB (hi + lo planes), W' ring
@@ -51,7 +52,19 @@ struct KFParams {
   int hi_policy;                 // L2 policy of the A-stream's hi plane: 0 evict_last, 1 normal, 2 evict_first
   int lag;                       // > 0: the A-stream starts round ρ only once the B-stream finished round ρ−lag−1
                                  // (bounds the X_hi rounds waiting in L2 for their re-read); 0: unbounded
+  int* err;                      // device error word: DEV_TIMEOUT if a sibling's tile flag never arrives
 };
+
+// Bound on one inter-CTA wait (a sibling's tile flag).  The kernel is launched cooperatively (all CTAs
+// co-resident, or the launch fails and the two-kernel pass runs instead), so the wait normally lasts well
+// under a pass; the bound turns a broken residency assumption into PPCA_ERR_CUDA instead of a hang.
+constexpr uint64_t kFlagTimeoutNs = 2000000000ull;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
@@ -187,7 +200,16 @@ __global__ void __launch_bounds__(kf::NTHREADS, 1)
         const int64_t t = tb + q / (BM / KR);
         const int h = (int)(q % (BM / KR));
         if (h == 0) {
-          while (ld_acquire_gpu(p.flags + t) != p.epoch) __nanosleep(32);
+          if (ld_acquire_gpu(p.flags + t) != p.epoch) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_gpu(p.flags + t) != p.epoch) {
+              __nanosleep(32);
+              if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+                atomicOr(p.err, DEV_TIMEOUT);
+                break;
+              }
+            }
+          }
           fence_proxy_async_global();             // Yᵀ was written by generic stores on another SM
         }
         const uint32_t s = q % NSTB, ph = (q / NSTB) & 1;

@@ -147,8 +147,8 @@ def test_power_priming_and_refine_parity(P, ctx, name, impl, split):
     """impl 2 runs the single-read fused power pass where eligible (split/bf16 X, m ≤ 64, d ≤ 1024: C3s
     split); impl 3 forces the two-kernel pass."""
     import torch
-    if impl >= 2 and name == "C1":
-        pytest.skip("auto keeps 0.5 MB shards on the fp32 SIMT pass (bf16 rounding of X at n=2000 ~1e-4)")
+    if impl >= 2 and name == "C1" and not split:
+        pytest.skip("plain-f32 tcgen05 on C1: test_gpu_r2.test_c1_forced_tcgen05_plain_f32_error_budget (R30)")
     w = C.SMALL[name]
     s = w.spec
     if split and s.dtype != "f32":
