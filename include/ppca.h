@@ -178,6 +178,13 @@ ppca_status ppca_prime_eigengame(ppca_ctx* ctx, const ppca_matrix* X, int m, int
 ppca_status ppca_refine(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k,
                         float* E, double* theta_host, int* subspace_dim);
 
+/* ppca_refine with flags.  PPCA_REFINE_ORTHONORMAL: the caller guarantees that the rows of V are orthonormal
+ * to fp32 rounding (e.g. the W returned by ppca_prime_power), so B = orth(V) is skipped (B = V; the Rayleigh–
+ * Ritz step uses the Gram of the operand rows, so θ and E stay those of span V); no rank check is made. */
+#define PPCA_REFINE_ORTHONORMAL 1u
+ppca_status ppca_refine_ex(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k, unsigned flags,
+                           float* E, double* theta_host, int* subspace_dim);
+
 /* Row-subsampled pPCA refinement (§5.2: "we only project 10% of the data for computing
  * full-PCA"; reading R25): as ppca_refine, but the projected covariance
  * is formed from the 128-row tiles of each shard whose Philox4x32-10 uniform (sample_seed, stream 7,
@@ -203,6 +210,18 @@ ppca_status ppca_refine_sampled(ppca_ctx* ctx, const ppca_matrix* X, const float
 ppca_status ppca_check_prop3(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, const float* T,
                              int upto, double tol, double* angles_host, int* flags_host);
 
+/* Theorem 1 as an online assertion (§4.2 Theorem 1 L308-312 with Prop. 3; SURVEY §8(f)
+ * NEXT-4): call at a priming checkpoint with the priming output V (device [m][d]; its first k rows, normalised,
+ * are e_i^PRIMING) and the true eigenvectors T (device [k][d]).  upto_out: length of the leading run of Prop. 3
+ * conditions that hold within `tol` (as ppca_check_prop3).  On that run pPCA's i-th vector is the vector of
+ * span V closest to e_i, so the theorem's conclusion is ∠(pPCA_i, e_i) ≤ ∠(e_i^PRIMING, e_i) (+ tol) —
+ * hence LCES(pPCA) ≥ LCES(priming) for every threshold.  ang_priming_host / ang_ppca_host: host double[k] out;
+ * holds_out: 1 iff the conclusion holds on the run (0 flags a violation).  Two passes over X (the checker's
+ * projected Gram and the refine).  Errors: as ppca_check_prop3 and ppca_refine. */
+ppca_status ppca_check_theorem1(ppca_ctx* ctx, const ppca_matrix* X, const float* V, int m, int k, const float* T,
+                                double tol, int* upto_out, double* ang_priming_host, double* ang_ppca_host,
+                                int* holds_out);
+
 /* Evaluation (§5.3): angle_i = arccos(min(1,|<E_i,T_i>|)) and
  * LCES(V) = #consecutive i from 1 with angle_i < V (strict), for each threshold.
  * E, T: device [k][d] unit rows.  angles_host: double[k]; lces_host: int[nthr]. */
@@ -213,10 +232,11 @@ ppca_status ppca_eval(ppca_ctx* ctx, const float* E, const float* T, int k, int6
  * res_host[i] = ‖XᵀX e_i − θ_i e_i‖₂ for the k rows e_i of E (device [k][d] fp32, unit rows) and
  * theta_host[i] (host double[k]).  By Weyl some eigenvalue of XᵀX lies within res_i of θ_i; with a gap δ
  * the angle to the true eigenvector is ≤ res_i/δ (Davis–Kahan).  One exact-fp32 CUDA-core pass over X
- * (no bf16 rounding of E or of X·Eᵀ), fp64 split-K sums, summed over ranks.  Untimed support, not a
- * step of the method.  Errors: INVALID_ARG (null pointers), as ppca_refine for X, k ≤ min(d, 128). */
+ * (no bf16 rounding of E or of X·Eᵀ), fp64 split-K sums, summed over ranks.  res_gram_host (optional, host
+ * double[k*k]): the Gram R·Rᵀ of the residual rows, so ‖R‖₂ = sqrt(λ_max) for the sinΘ bound ‖R‖₂/δ.  Untimed
+ * support, not a step of the method.  Errors: INVALID_ARG (null pointers), as ppca_refine for X, k ≤ min(d, 128). */
 ppca_status ppca_ritz_residuals(ppca_ctx* ctx, const ppca_matrix* X, const float* E, int k,
-                                const double* theta_host, double* res_host);
+                                const double* theta_host, double* res_host, double* res_gram_host);
 
 /* Captured variance vᵀ(XᵀX)v = ‖Xv‖² for each row of V (PAPER.md L416 footnote),
  * summed over ranks.  var_host: double[m]. */

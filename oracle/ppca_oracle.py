@@ -361,6 +361,27 @@ def check_prop3(X: np.ndarray, V: np.ndarray, T: np.ndarray, upto: int, tol: flo
     return flags, np.array(angs)
 
 
+def theorem1_check(X: np.ndarray, V: np.ndarray, T: np.ndarray, k: int, tol: float = 1e-8):
+    """Theorem 1 (P L308-312) as an online assertion: for the priming output V (m ≥ k
+    vectors, e_i^PRIMING = v_i/‖v_i‖ for i ≤ k) and the true eigenvectors T, let `upto` be the length of the
+    leading run of Proposition 3's conditions that hold (check_prop3 flags, P L293-302).  On that run the
+    full-PCA step returns π_S(e_i)/‖π_S(e_i)‖ as its i-th vector (Prop. 1 / Prop. 3's proof, P L287-306) —
+    the vector of S closest to e_i — so it cannot be farther from e_i than the priming's own v_i ∈ S:
+        ∠(pPCA_i, e_i) ≤ ∠(v_i, e_i) + tol   for every i ≤ upto,
+    hence LCES(pPCA) ≥ LCES(priming) on that run for every threshold V.  Returns (upto, angles of the priming
+    vectors, angles of the pPCA vectors, holds)."""
+    flags, _ = check_prop3(X, V, T, k, tol)
+    upto = 0
+    while upto < k and flags[upto]:
+        upto += 1
+    E, _, _, _ = ppca_refine(X, V, k)
+    Vn = normalize_rows(np.asarray(V, dtype=np.float64)[:k])
+    a_prim = angles(Vn, T[:k])
+    a_ppca = angles(E, T[:k])
+    holds = all(a_ppca[i] <= a_prim[i] + tol for i in range(upto))
+    return upto, a_prim, a_ppca, holds
+
+
 def ritz_values(S: np.ndarray) -> np.ndarray:
     """Ritz values of an orthonormal-basis Gram S (the pPCA eigenvalue estimates)."""
     return jacobi_eigh(S)[0]

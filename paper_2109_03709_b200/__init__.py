@@ -31,7 +31,8 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
            "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
-           "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals"]
+           "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals", "ppca_refine_ex",
+           "ppca_check_theorem1"]
 
 
 class PPCAError(RuntimeError):
@@ -78,7 +79,10 @@ def load(path: str = LIB_PATH):
         "ppca_generate": (I, [P, ctypes.POINTER(ppca_gen_spec), P, I64, ctypes.POINTER(I64), P]),
         "ppca_prime_power": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, ctypes.c_uint64, P, P, ctypes.POINTER(I)]),
         "ppca_collective_count": (I64, [P]),
-        "ppca_ritz_residuals": (I, [P, ctypes.POINTER(ppca_matrix), P, I, P, P]),
+        "ppca_ritz_residuals": (I, [P, ctypes.POINTER(ppca_matrix), P, I, P, P, P]),
+        "ppca_check_theorem1": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, P, D, ctypes.POINTER(I), P, P,
+                                    ctypes.POINTER(I)]),
+        "ppca_refine_ex": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, ctypes.c_uint, P, P, ctypes.POINTER(I)]),
         "ppca_experiments_enabled": (I, []),
         "ppca_prime_oja": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, D, I64, ctypes.c_uint64, P, P,
                                ctypes.POINTER(I64)]),
@@ -330,6 +334,17 @@ def ppca_refine(ctx, X: ppca_matrix, V, m: int, k: int, E) -> tuple[np.ndarray, 
     return theta, dim.value
 
 
+PPCA_REFINE_ORTHONORMAL = 1
+
+
+def ppca_refine_ex(ctx, X: ppca_matrix, V, m: int, k: int, E, flags: int = 0) -> tuple[np.ndarray, int]:
+    theta = np.zeros(k, dtype=np.float64)
+    dim = ctypes.c_int()
+    _check(ctx, load().ppca_refine_ex(ctx, ctypes.byref(X), _ptr(V), m, k, flags, _ptr(E), _np_ptr(theta),
+                                      ctypes.byref(dim)), "ppca_refine_ex")
+    return theta, dim.value
+
+
 def ppca_refine_sampled(ctx, X: ppca_matrix, V, m: int, k: int, E, fraction: float,
                         sample_seed: int) -> tuple[np.ndarray, int, int]:
     """Row-subsampled refine: (θ rescaled to the full data, subspace dim, rows used)."""
@@ -351,6 +366,16 @@ def ppca_check_prop3(ctx, X: ppca_matrix, V, m: int, T, upto: int, tol: float = 
     return [bool(f) for f in fl], ang
 
 
+def ppca_check_theorem1(ctx, X: ppca_matrix, V, m: int, k: int, T, tol: float = 1e-8):
+    """Theorem 1 online assertion (P L308-312): (upto, priming angles, pPCA angles, holds)."""
+    upto, holds = ctypes.c_int(), ctypes.c_int()
+    ap = np.zeros(k, dtype=np.float64)
+    aq = np.zeros(k, dtype=np.float64)
+    _check(ctx, load().ppca_check_theorem1(ctx, ctypes.byref(X), _ptr(V), m, k, _ptr(T), tol, ctypes.byref(upto),
+                                           _np_ptr(ap), _np_ptr(aq), ctypes.byref(holds)), "ppca_check_theorem1")
+    return upto.value, ap, aq, bool(holds.value)
+
+
 def ppca_eval(ctx, E, T, k: int, d: int, thresholds) -> tuple[np.ndarray, np.ndarray]:
     thr = np.ascontiguousarray(thresholds, dtype=np.float64)
     ang = np.zeros(k, dtype=np.float64)
@@ -360,13 +385,15 @@ def ppca_eval(ctx, E, T, k: int, d: int, thresholds) -> tuple[np.ndarray, np.nda
     return ang, lc
 
 
-def ppca_ritz_residuals(ctx, X: ppca_matrix, E, k: int, theta) -> np.ndarray:
-    """‖XᵀX e_i − θ_i e_i‖ for the rows of E (certification support, reading R29)."""
+def ppca_ritz_residuals(ctx, X: ppca_matrix, E, k: int, theta, gram: bool = False):
+    """‖XᵀX e_i − θ_i e_i‖ for the rows of E (certification support, reading R29); gram=True also returns the
+    k×k Gram of the residual rows (‖R‖₂² = its largest eigenvalue)."""
     th = np.ascontiguousarray(theta[:k], dtype=np.float64)
     out = np.zeros(k, dtype=np.float64)
-    _check(ctx, load().ppca_ritz_residuals(ctx, ctypes.byref(X), _ptr(E), k, _np_ptr(th), _np_ptr(out)),
-           "ppca_ritz_residuals")
-    return out
+    rg = np.zeros((k, k), dtype=np.float64) if gram else None
+    _check(ctx, load().ppca_ritz_residuals(ctx, ctypes.byref(X), _ptr(E), k, _np_ptr(th), _np_ptr(out),
+                                           _np_ptr(rg) if gram else None), "ppca_ritz_residuals")
+    return (out, rg) if gram else out
 
 
 def ppca_captured_variance(ctx, X: ppca_matrix, V, m: int) -> np.ndarray:

@@ -591,7 +591,7 @@ ppca_status ppca_prime_eigengame(ppca_ctx* h, const ppca_matrix* X, int m, int b
 // of the data"; reading R25) and θ are rescaled by n_global / rows used.
 static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int m, int k, double fraction,
                                uint64_t sample_seed, float* E, double* theta_host, int* subspace_dim,
-                               int64_t* rows_used) {
+                               int64_t* rows_used, unsigned flags = 0) {
   PPCA_TRY(check_matrix(c, X, m));
   if (!V || !E || k < 1 || k > m) return set_error(c, PPCA_ERR_INVALID_ARG, "bad refine args (k=%d, m=%d)", k, m);
   if (!(fraction > 0.0)) return set_error(c, PPCA_ERR_INVALID_ARG, "sample fraction must be > 0");
@@ -631,15 +631,23 @@ static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int
     PPCA_TRY(check_cuda(c, cudaStreamSynchronize(c->stream), "count"));
   }
   if (sampled && rows_total <= 0.0) return set_error(c, PPCA_ERR_INVALID_ARG, "the row sample is empty");
-  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream), "copy V"));
-  PPCA_TRY(normalize_rows(c, B, m, d));                 // current_components
   int mm = m;
-  // B = orth(V); a direction whose relative residual is < 1e-6 is dropped (SPEC L51 drops < 1e-10 in
-  // fp64; fp32 inputs cannot resolve residuals below ~1e-7 — DESIGN.md reading R14)
-  PPCA_TRY(cholqr2(c, B, m, d, 1e-6, &mm));
-  if (mm < k) {
-    finish(c, "ppca_refine");
-    return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "only %d of %d directions survive", mm, k);
+  if (flags & PPCA_REFINE_ORTHONORMAL) {
+    // the caller guarantees orthonormal rows (ppca_prime_power's W): B = V.  The Rayleigh–Ritz step is the
+    // generalized one with the Gram of the operand rows, so θ and E are exact for span V regardless
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                        "copy V"));
+  } else {
+    PPCA_TRY(check_cuda(c, cudaMemcpyAsync(B, V, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                        "copy V"));
+    PPCA_TRY(normalize_rows(c, B, m, d));                 // current_components
+    // B = orth(V); a direction whose relative residual is < 1e-6 is dropped (SPEC L51 drops < 1e-10 in
+    // fp64; fp32 inputs cannot resolve residuals below ~1e-7 — DESIGN.md reading R14)
+    PPCA_TRY(cholqr2(c, B, m, d, 1e-6, &mm));
+    if (mm < k) {
+      finish(c, "ppca_refine");
+      return set_error(c, PPCA_ERR_SUBSPACE_COLLAPSE, "only %d of %d directions survive", mm, k);
+    }
   }
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, mm, &plan));
@@ -676,6 +684,14 @@ ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m
   if (!h) return PPCA_ERR_INVALID_ARG;
   cudaSetDevice(h->c.device);
   return refine_impl(&h->c, X, V, m, k, 1.0, 0, E, theta_host, subspace_dim, nullptr);
+}
+
+ppca_status ppca_refine_ex(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, unsigned flags, float* E,
+                           double* theta_host, int* subspace_dim) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  if (flags & ~(unsigned)PPCA_REFINE_ORTHONORMAL) return set_error(&h->c, PPCA_ERR_INVALID_ARG, "unknown refine flags");
+  cudaSetDevice(h->c.device);
+  return refine_impl(&h->c, X, V, m, k, 1.0, 0, E, theta_host, subspace_dim, nullptr, flags);
 }
 
 ppca_status ppca_refine_sampled(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, double fraction,
@@ -734,6 +750,51 @@ ppca_status ppca_check_prop3(ppca_ctx* h, const ppca_matrix* X, const float* V, 
   return PPCA_OK;
 }
 
+// ---------------------------------------------------------------------------- Theorem 1 assertion (NEXT-4)
+// P L308-312 with Prop. 3 (L293-302): upto = the leading run of Prop. 3 conditions that hold; on it pPCA's i-th
+// vector is π_S(e_i)/‖π_S(e_i)‖, the vector of S closest to e_i, so ∠(pPCA_i, e_i) ≤ ∠(v_i, e_i) (+ tol).
+ppca_status ppca_check_theorem1(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, const float* T,
+                                double tol, int* upto_out, double* ang_priming_host, double* ang_ppca_host,
+                                int* holds_out) {
+  if (!h) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  if (!V || !T || !upto_out || !ang_priming_host || !ang_ppca_host || !holds_out || k < 1 || k > m || !(tol >= 0.0))
+    return set_error(c, PPCA_ERR_INVALID_ARG, "bad check_theorem1 args (k=%d, m=%d)", k, m);
+  std::vector<double> cang(k);
+  std::vector<int> flags(k);
+  PPCA_TRY(ppca_check_prop3(h, X, V, m, T, k, tol, cang.data(), flags.data()));
+  int upto = 0;
+  while (upto < k && flags[upto]) ++upto;
+  const int64_t d = X->d;
+  float* buf = (float*)scratch(c, S_P3F, (size_t)2 * k * d * sizeof(float));
+  double* dots = (double*)scratch(c, S_ROWRED, (size_t)2 * std::max(k, PPCA_MAX_M) * sizeof(double));
+  if (!buf || !dots) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  float* E = buf;
+  float* Vn = buf + (size_t)k * d;
+  std::vector<double> th(k);
+  int dim = 0;
+  PPCA_TRY(refine_impl(c, X, V, m, k, 1.0, 0, E, th.data(), &dim, nullptr));
+  PPCA_TRY(check_cuda(c, cudaMemcpyAsync(Vn, V, (size_t)k * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
+                      "copy V"));
+  PPCA_TRY(normalize_rows(c, Vn, k, d));                  // e_i^PRIMING = v_i / ‖v_i‖
+  PPCA_TRY(row_dots(c, Vn, T, k, d, dots));
+  PPCA_TRY(row_dots(c, E, T, k, d, dots + k));
+  PPCA_TRY(finish(c, "ppca_check_theorem1"));
+  std::vector<double> hd(2 * k);
+  if (cudaMemcpy(hd.data(), dots, 2 * k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy dots");
+  int holds = 1;
+  for (int i = 0; i < k; ++i) {
+    ang_priming_host[i] = acos(std::min(1.0, fabs(hd[i])));
+    ang_ppca_host[i] = acos(std::min(1.0, fabs(hd[k + i])));
+    if (i < upto && ang_ppca_host[i] > ang_priming_host[i] + tol) holds = 0;
+  }
+  *upto_out = upto;
+  *holds_out = holds;
+  return PPCA_OK;
+}
+
 // ---------------------------------------------------------------------------- eval / support
 ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_t d, const double* thr_host, int nthr,
                       double* angles_host, int* lces_host) {
@@ -761,7 +822,7 @@ ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_
 // Certification support (reading R29): residual norms of Ritz pairs, one exact-fp32 SIMT
 // pass (Y = X·Eᵀ, Z = YᵀX with fp64 split-K sums; no bf16 rounding of E or Y), all-reduced.
 ppca_status ppca_ritz_residuals(ppca_ctx* h, const ppca_matrix* X, const float* E, int k, const double* theta_host,
-                                double* res_host) {
+                                double* res_host, double* res_gram_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
   cudaSetDevice(c->device);
@@ -782,9 +843,18 @@ ppca_status ppca_ritz_residuals(ppca_ctx* h, const ppca_matrix* X, const float* 
   PPCA_TRY(check_cuda(c, cudaMemcpyAsync(buf, theta_host, (size_t)k * sizeof(double), cudaMemcpyHostToDevice,
                                          c->stream), "copy theta"));
   PPCA_TRY(ritz_resid(c, Z, E, buf, k, d, buf + k));
+  double* RG = nullptr;
+  if (res_gram_host) {                                   // R R^T of the residual rows R_i = Z_i − θ_i E_i (in Z)
+    RG = (double*)scratch(c, S_GRAM, (size_t)k * k * sizeof(double));
+    if (!RG) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    PPCA_TRY(resid_rows(c, Z, E, buf, k, d));
+    PPCA_TRY(vec_gram(c, Z, k, d, RG));
+  }
   PPCA_TRY(finish(c, "ppca_ritz_residuals"));
   if (cudaMemcpy(res_host, buf + k, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
     return set_error(c, PPCA_ERR_CUDA, "copy residuals");
+  if (res_gram_host && cudaMemcpy(res_gram_host, RG, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_error(c, PPCA_ERR_CUDA, "copy residual Gram");
   return PPCA_OK;
 }
 

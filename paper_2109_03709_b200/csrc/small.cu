@@ -138,11 +138,22 @@ __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __re
   }
 }
 
+// short d (fewer GK-column stages than SMs, e.g. C3's 32) or m > 128: the 32×32-tile kernel over
+// (tile, tile, split) keeps more CTAs busy (7.4 vs 9.3 µs at d = 1024, m = 64); otherwise the 8×8-register-tile
+// kernel over one d-slab per SM
+static bool gram_short(const Ctx* c, int m, int64_t d) { return m > 128 || ceil_div(d, (int64_t)GK) < c->sm_count; }
+
 static void vec_gram_split(const Ctx* c, int m, int64_t d, int* nsplit_out, int64_t* cps_out) {
-  (void)m;
-  const int64_t stages = ceil_div(d, (int64_t)GK);
-  const int64_t want = std::min<int64_t>(stages, (int64_t)c->sm_count);
-  const int64_t cps = ceil_div(stages, want) * GK;
+  int64_t cps;
+  if (gram_short(c, m, d)) {
+    const int tiles = (int)ceil_div(m, 32);
+    const int64_t want = ceil_div(2 * (int64_t)c->sm_count, (int64_t)tiles * tiles);
+    const int64_t ns = std::max<int64_t>(1, std::min(want, ceil_div(d, (int64_t)64)));
+    cps = ceil_div(ceil_div(d, ns), (int64_t)64) * 64;
+  } else {
+    const int64_t stages = ceil_div(d, (int64_t)GK);
+    cps = ceil_div(stages, std::min<int64_t>(stages, (int64_t)c->sm_count)) * GK;
+  }
   *nsplit_out = (int)ceil_div(d, cps);
   *cps_out = cps;
 }
@@ -166,17 +177,16 @@ ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cud
   double* P = (double*)scratch(c, part_slot, (size_t)nsplit * m * m * sizeof(double));
   if (!P) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   const int mb = (int)ceil_div(m, 8);
-  if (mb <= 1) launch_gram_mb<1>(nsplit, st, V, m, d, cps, P);
+  if (gram_short(c, m, d)) {
+    const int tiles = (int)ceil_div(m, 32);
+    vec_gram_generic_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
+  } else if (mb <= 1) launch_gram_mb<1>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 2) launch_gram_mb<2>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 4) launch_gram_mb<4>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 6) launch_gram_mb<6>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 8) launch_gram_mb<8>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 12) launch_gram_mb<12>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 16) launch_gram_mb<16>(nsplit, st, V, m, d, cps, P);
-  else {
-    const int tiles = (int)ceil_div(m, 32);
-    vec_gram_generic_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
-  }
   PPCA_LAUNCH_CHECK(c, "vec_gram");
   return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G, st);
 }
@@ -366,7 +376,8 @@ static const bool g_chol_reg = tune_env("PPCA_CHOL_REG", 1) != 0;
 // below and by the Ritz kernels (ritz.cuh) for the operand Gram's L⁻¹.
 template <int CQ>
 __device__ void chol_inv_sweep(const double* __restrict__ G, int m, double* __restrict__ Linv, int ldl,
-                               int* __restrict__ keep, int* d_err) {
+                               int* __restrict__ keep, int* d_err, int ldg = -1) {
+  if (ldg < 0) ldg = m;
   __shared__ double colb[2][CF_M];
   __shared__ double rowb[2][CF_M];
   constexpr int NQ = CF_M / CQ;
@@ -375,7 +386,7 @@ __device__ void chol_inv_sweep(const double* __restrict__ G, int m, double* __re
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int k = cp + CQ * q;
-    a[q] = (i < m && k < m) ? G[i * m + k] : (i == k ? 1.0 : 0.0);
+    a[q] = (i < m && k < m) ? G[i * ldg + k] : (i == k ? 1.0 : 0.0);
     mm_[q] = i == k ? 1.0 : 0.0;
   }
   // step 0's buffers
@@ -436,9 +447,83 @@ __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __r
   if (threadIdx.x == 0) *m_out = m;
 }
 
+// 64 < m ≤ 128 (C5's m = 128): 2×2 blocks of 64 around the register sweep, one CTA of 512 threads —
+//   L11⁻¹ = sweep(A11);  L21 = A21·L11⁻ᵀ;  A22' = A22 − L21·L21ᵀ;  L22⁻¹ = sweep(A22');
+//   L⁻¹ = [[L11⁻¹, 0], [−L22⁻¹·L21·L11⁻¹, L22⁻¹]]
+// (four 64³ fp64 products in shared memory between two sweeps; the one-CTA blocked elimination it replaces
+// took 153 µs at m = 128).
+constexpr int BK64 = 64, BKL = BK64 + 1;
+__device__ __forceinline__ void mm64(const double* __restrict__ A, bool at, const double* __restrict__ B, bool bt,
+                                     double* __restrict__ C, double alpha, const double* __restrict__ Cin, int ldcin) {
+  // C[i][j] = Cin[i][j] + alpha·Σ_k opA[i][k]·opB[k][j]  (64×64, ld BKL; op = transpose when flagged; Cin may be
+  // null); 512 threads × 8 outputs, rows i = t/8, columns j = t%8 + 8q
+  const int i = threadIdx.x >> 3, j0 = threadIdx.x & 7;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int k = 0; k < BK64; ++k) {
+    const double a = at ? A[k * BKL + i] : A[i * BKL + k];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fma(a, bt ? B[(j0 + 8 * q) * BKL + k] : B[k * BKL + j0 + 8 * q], acc[q]);
+  }
+  __syncthreads();                                 // C may alias an operand's storage of an earlier phase
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int j = j0 + 8 * q;
+    C[i * BKL + j] = (Cin ? Cin[i * ldcin + j] : 0.0) + alpha * acc[q];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) chol_inv_blk_kernel(const double* __restrict__ G, int m, double* __restrict__ Linv,
+                                                           int* __restrict__ row_map, int* __restrict__ m_out,
+                                                           int* d_err) {
+  extern __shared__ double cb[];
+  double* L11i = cb;                              // L11⁻¹
+  double* L21 = L11i + BK64 * BKL;                  // A21, then L21
+  double* A22 = L21 + BK64 * BKL;                   // A22', then T = L21·L11⁻¹
+  double* L22i = A22 + BK64 * BKL;                  // L22⁻¹
+  const int m2 = m - BK64;
+  chol_inv_sweep<8>(G, BK64, L11i, BKL, nullptr, d_err, m);
+  for (int e = threadIdx.x; e < BK64 * BK64; e += 512) {            // A21 (rows ≥ m2 zero)
+    const int i = e / BK64, k = e % BK64;
+    A22[i * BKL + k] = i < m2 ? G[(BK64 + i) * m + k] : 0.0;
+  }
+  __syncthreads();
+  mm64(A22, false, L11i, true, L21, 1.0, nullptr, 0);            // L21 = A21·L11⁻ᵀ
+  for (int e = threadIdx.x; e < BK64 * BK64; e += 512) {            // A22 (identity beyond m2)
+    const int i = e / BK64, k = e % BK64;
+    L22i[i * BKL + k] = (i < m2 && k < m2) ? G[(BK64 + i) * m + BK64 + k] : (i == k ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  mm64(L21, false, L21, true, A22, -1.0, L22i, BKL);             // A22' = A22 − L21·L21ᵀ
+  chol_inv_sweep<8>(A22, m2, L22i, BKL, nullptr, d_err, BKL);
+  mm64(L21, false, L11i, false, A22, 1.0, nullptr, 0);           // T = L21·L11⁻¹
+  mm64(L22i, false, A22, false, L21, -1.0, nullptr, 0);          // X21 = −L22⁻¹·T
+  for (int e = threadIdx.x; e < m * m; e += 512) {
+    const int i = e / m, k = e % m;
+    double v;
+    if (i < BK64) v = k < BK64 ? L11i[i * BKL + k] : 0.0;
+    else v = k < BK64 ? L21[(i - BK64) * BKL + k] : L22i[(i - BK64) * BKL + (k - BK64)];
+    Linv[e] = v;
+  }
+  if (threadIdx.x < m) row_map[threadIdx.x] = threadIdx.x;
+  if (threadIdx.x == 0) *m_out = m;
+}
+
 static int g_chol_cq = tune_env("PPCA_CHOL_CQ", 8);
 static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_map, int* m_out, int* d_err,
                                 cudaStream_t st) {
+  if (m > CF_M) {
+    const size_t smem = (size_t)4 * BK64 * BKL * sizeof(double);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static uint64_t attr = 0;
+    if (first_on_device(&attr, dev))
+      cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    chol_inv_blk_kernel<<<1, 512, smem, st>>>(G, m, Linv, row_map, m_out, d_err);
+    return;
+  }
   if (g_chol_cq == 4)
     chol_inv_reg_kernel<4><<<1, 256, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
   else if (g_chol_cq == 16)
@@ -454,15 +539,74 @@ static size_t chol_inv_smem(int m) {
 }
 
 // ============================================================================ apply: OUT = C · IN
-// OUT[map(i)][x] = Σ_j C[i][j] IN[j][x]  (j ≤ i if lower), fp64 accumulate.  One CTA per 32 columns: the
-// rows × m_in block of C (fp64) and the m_in × 32 slab of IN are staged in shared memory with every load
-// in flight at once (the inner loop then never waits on L2), warp w computes rows i ≡ w (mod 8) with
-// lane = column (C[i][j] a shared-memory broadcast).
 // OUT[row_map(i)] = Σ_j C[i][j]·IN[j] for i < rows (C fp64 [rows][ldc], IN [m_in][d] fp32, fp64 accumulation;
 // lower: C lower-triangular).  The apply of CholQR (W = L⁻¹Z, d·m²/2 MAC), the lift E = R·B and the EigenGame
 // mixing.  fp64-FMA bound: a grid of ≤ one CTA per SM, each holding Cᵀ in shared memory once and sweeping
 // 32-column chunks of IN; thread = RPT rows × 4 columns of the output chunk (RPT + 4 operand loads per 4·RPT
 // DFMA, warp-broadcast), the next chunk's IN loaded into registers while the current one is consumed.
+// short d (fewer 32-column chunks than SMs, e.g. C3's d = 1024): one CTA per 32 columns × row blocks, C
+// staged per CTA (measured faster there than the chunk-sweeping kernel below: 8.1 vs 11.6 µs for m = 64)
+constexpr int AP_COLS = 32;
+__global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
+                                                         int m_in, const int* __restrict__ row_map,
+                                                         bool lower, const float* __restrict__ IN,
+                                                         int64_t d, float* __restrict__ OUT, int rows_per_cta) {
+  extern __shared__ double cs[];                 // this CTA's rows × m_in (fp64), then m_in × AP_COLS (fp32)
+  const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  float* ins = reinterpret_cast<float*>(cs + (size_t)rows_per_cta * m_in);
+  const int64_t x0 = (int64_t)blockIdx.x * AP_COLS;
+  copy_batched<16>(threadIdx.x, (r1 - r0) * m_in, blockDim.x,
+                   [&](int64_t e) { return C[(r0 + e / m_in) * ldc + e % m_in]; },
+                   [&](int64_t e, double v) { cs[e] = v; });
+  copy_batched<8>(threadIdx.x, m_in * AP_COLS, blockDim.x,
+                  [&](int64_t e) {
+                    const int64_t x = x0 + e % AP_COLS;
+                    return IN[(e / AP_COLS) * d + (x < d ? x : d - 1)];
+                  },
+                  [&](int64_t e, float v) { ins[e] = x0 + e % AP_COLS < d ? v : 0.f; });
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t x = x0 + lane;
+  for (int i = r0 + warp; i < r1; i += 8) {
+    const int oi = row_map ? row_map[i] : i;
+    if (oi < 0) continue;
+    const double* crow = cs + (size_t)(i - r0) * m_in;
+    const int jend = lower ? min(i + 1, m_in) : m_in;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: the FMA latency is hidden
+    int j = 0;
+    for (; j + 4 <= jend; j += 4) {
+      a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
+      a1 = fma(crow[j + 1], (double)ins[(j + 1) * AP_COLS + lane], a1);
+      a2 = fma(crow[j + 2], (double)ins[(j + 2) * AP_COLS + lane], a2);
+      a3 = fma(crow[j + 3], (double)ins[(j + 3) * AP_COLS + lane], a3);
+    }
+    for (; j < jend; ++j) a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
+    if (x < d) OUT[(int64_t)oi * d + x] = (float)((a0 + a1) + (a2 + a3));
+  }
+}
+
+static ppca_status apply_rows_small(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
+                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  // row blocks (multiples of 8 rows) until the grid covers the SMs: d = 1024 alone gives 32 CTAs
+  const int64_t gx = ceil_div(d, (int64_t)AP_COLS);
+  static const bool split = !(getenv("PPCA_APPLY_SPLIT") && atoi(getenv("PPCA_APPLY_SPLIT")) == 0);
+  int rpc = rows;
+  if (split && gx < c->sm_count) {
+    const int gy = (int)std::min<int64_t>(ceil_div((int64_t)c->sm_count, gx), ceil_div((int64_t)rows, (int64_t)8));
+    rpc = (int)ceil_div((int64_t)ceil_div((int64_t)rows, (int64_t)gy), (int64_t)8) * 8;
+  }
+  const unsigned gy = (unsigned)ceil_div((int64_t)rows, (int64_t)rpc);
+  size_t smem = (size_t)rpc * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
+  apply_rows_kernel<<<dim3((unsigned)gx, gy), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
+  PPCA_LAUNCH_CHECK(c, "apply_rows");
+  return PPCA_OK;
+}
+
 constexpr int AT_COLS = 32;
 
 template <int RPT>
@@ -563,6 +707,8 @@ static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_
                               bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
   if (rows < 1 || m_in < 1 || d < 1) return PPCA_OK;
   if (rows > 128 || m_in > 128) return set_error(c, PPCA_ERR_UNSUPPORTED, "apply: %d x %d > 128", rows, m_in);
+  if (ceil_div(d, (int64_t)AT_COLS) < 2 * c->sm_count)
+    return apply_rows_small(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   if (rows <= 32) launch_apply_tiled<1>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   else if (rows <= 64) launch_apply_tiled<2>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   else launch_apply_tiled<4>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
@@ -576,7 +722,7 @@ ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_m
   if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
-  if (m <= CF_M && g_chol_reg) {
+  if (m <= 2 * CF_M && g_chol_reg) {
     launch_chol_inv_reg(G, m, Linv, row_map, m_out, c->d_err, st);
   } else {
     const size_t smem = chol_inv_smem(m);
@@ -613,7 +759,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   const size_t smem = chol_inv_smem(m);
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
     PPCA_TRY(vec_gram(c, Zin, m, d, G));
-    if (m <= CF_M && g_chol_reg)
+    if (m <= 2 * CF_M && g_chol_reg)
       launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
       chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
@@ -628,7 +774,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   for (int pass = 0; pass < passes; ++pass) {
     PPCA_TRY(vec_gram(c, W, m, d, G));
     const double dt = pass == 0 ? drop_tol : 0.0;
-    if (dt <= 0.0 && m <= CF_M && g_chol_reg)
+    if (dt <= 0.0 && m <= 2 * CF_M && g_chol_reg)
       launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
       chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, dt, Linv, row_map, d_mout, c->d_err);
@@ -1124,6 +1270,22 @@ __global__ void ritz_resid_kernel(const float* __restrict__ Z, const float* __re
 ppca_status ritz_resid(Ctx* c, const float* Z, const float* E, const double* theta, int k, int64_t d, double* res) {
   ritz_resid_kernel<<<k, 256, 0, c->stream>>>(Z, E, theta, d, res);
   PPCA_LAUNCH_CHECK(c, "ritz_resid");
+  return PPCA_OK;
+}
+
+// Z_i ← Z_i − θ_i E_i in place (fp32 result of an fp64 difference)
+__global__ void resid_rows_kernel(float* __restrict__ Z, const float* __restrict__ E, const double* __restrict__ theta,
+                                  int64_t d) {
+  float* z = Z + (int64_t)blockIdx.y * d;
+  const float* e = E + (int64_t)blockIdx.y * d;
+  const double th = theta[blockIdx.y];
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < d; x += (int64_t)gridDim.x * blockDim.x)
+    z[x] = (float)((double)z[x] - th * (double)e[x]);
+}
+
+ppca_status resid_rows(Ctx* c, float* Z, const float* E, const double* theta, int k, int64_t d) {
+  resid_rows_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(d, 256), 64), (unsigned)k), 256, 0, c->stream>>>(Z, E, theta, d);
+  PPCA_LAUNCH_CHECK(c, "resid_rows");
   return PPCA_OK;
 }
 

@@ -58,5 +58,7 @@ ppca_status prop3_device(Ctx* c, const double* G, int g, const double* S, int mm
 ppca_status row_dots(Ctx* c, const float* E, const float* T, int k, int64_t d, double* dots);
 // res[i] = ‖Z_i − θ_i E_i‖ (fp64), θ device double[k]
 ppca_status ritz_resid(Ctx* c, const float* Z, const float* E, const double* theta, int k, int64_t d, double* res);
+// Z_i ← Z_i − θ_i E_i in place
+ppca_status resid_rows(Ctx* c, float* Z, const float* E, const double* theta, int k, int64_t d);
 
 }  // namespace ppca

@@ -377,8 +377,61 @@ def test_ritz_residuals_match_oracle_c5s(P, ctx):
     P.ppca_prime_power(ctx, Xm, w.m, 2, w.init_seed, W)
     E = torch.zeros((k, s.d), dtype=torch.float32, device="cuda")
     th, _ = P.ppca_refine(ctx, Xm, W, w.m, k, E)
-    r = P.ppca_ritz_residuals(ctx, Xm, E, k, th)
+    r, rg = P.ppca_ritz_residuals(ctx, Xm, E, k, th, gram=True)
+    np.testing.assert_allclose(np.sqrt(np.diag(rg)), r, rtol=1e-4)           # the Gram of the same residual rows
+    R_ref = (X64 @ E_ref.T).T @ X64 - th_ref[:, None] * E_ref
+    assert np.sqrt(np.linalg.eigvalsh(rg)[-1]) == pytest.approx(np.linalg.norm(R_ref, 2), rel=2e-2)
     print(f"\n[R29] C5s residuals / θ1: oracle {np.min(r_ref) / th_ref[0]:.2e} … {np.max(r_ref) / th_ref[0]:.2e}, "
           f"max rel diff {np.max(np.abs(r - r_ref) / r_ref):.2e}")
     np.testing.assert_allclose(r, r_ref, rtol=2e-2)
     assert np.max(r_ref) > 1e-3 * th_ref[0]              # a non-converged block: residuals far above rounding
+
+
+def test_refine_orthonormal_flag_vs_oracle(P, ctx):
+    """ppca_refine_ex(PPCA_REFINE_ORTHONORMAL) on ppca_prime_power's W (orthonormal rows): B = orth(V) skipped,
+    the generalized Rayleigh–Ritz keeps θ and E those of span W — against the oracle's refine of its own priming,
+    and against the flag-less refine."""
+    import torch
+    w = C.SMALL["C3s"]
+    s = w.spec
+    Xs = G.dataset(s)
+    X64 = G.stored_to_f64(Xs, s.dtype)
+    lam, T = O.truth(X64)
+    W_ref, _ = O.prime_power(X64, G.init_gaussians(w.init_seed, w.m, s.d), w.iters)
+    E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, W_ref, w.k)
+    Xm = _device(P, ctx, Xs, s, True)
+    W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+    P.ppca_prime_power(ctx, Xm, w.m, w.iters, w.init_seed, W)
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    th, dim = P.ppca_refine_ex(ctx, Xm, W, w.m, w.k, E, P.PPCA_REFINE_ORTHONORMAL)
+    assert dim == w.m
+    U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, 1e-4, "C3s refine_ex", th_all_ref)
+    E2 = torch.zeros_like(E)
+    th2, _ = P.ppca_refine(ctx, Xm, W, w.m, w.k, E2)
+    assert U.ritz_rel_err(th, th2) < 1e-6
+    with pytest.raises(P.PPCAError):
+        P.ppca_refine_ex(ctx, Xm, W, w.m, w.k, E, 4)       # unknown flag
+
+
+def test_theorem1_assertion_vs_oracle(P, ctx):
+    """Theorem 1 online assertion (P L308-312, NEXT-4) on the device against the oracle: near-converged primings
+    of C3s (V = truth + δ·noise): the same leading run of Prop. 3 conditions, the same angles, and the conclusion
+    (pPCA no farther from e_i than the priming on that run) holds on both sides."""
+    import torch
+    w = C.SMALL["C3s"]
+    s = w.spec
+    Xs = G.dataset(s)
+    X64 = G.stored_to_f64(Xs, s.dtype)
+    lam, T = O.truth(X64)
+    Xm = _device(P, ctx, Xs, s, True)
+    k, m = 8, 16
+    Tt = torch.from_numpy(T[:k].astype(np.float32)).cuda()
+    for delta in [1e-3, 3e-2]:
+        V32 = (T[:m] + delta * np.random.default_rng(3).standard_normal((m, s.d)) / math.sqrt(s.d)).astype(np.float32)
+        up_ref, ap_ref, aq_ref, holds_ref = O.theorem1_check(X64, V32.astype(np.float64), T, k, tol=1e-4)
+        up, ap, aq, holds = P.ppca_check_theorem1(ctx, Xm, torch.from_numpy(V32).cuda(), m, k, Tt, 1e-4)
+        print(f"\n[theorem1] delta {delta}: run {up} (oracle {up_ref}), holds {holds}")
+        assert up == up_ref and holds and holds_ref
+        # angles from fp32 unit rows (acos of |⟨e, t⟩|): resolved to ~5e-4 near zero
+        np.testing.assert_allclose(ap, ap_ref, atol=1e-3)
+        np.testing.assert_allclose(aq, aq_ref, atol=1e-3)

@@ -133,3 +133,41 @@ def test_ritz_residuals_closed_form():
         assert r == pytest.approx((lam[0] - lam[1]) * abs(math.sin(a) * math.cos(a)), abs=1e-14)
     # a wrong θ shows up in full: ‖(M − θ')e‖ at an exact eigenvector
     assert O.ritz_residuals(X, np.array([[1.0, 0.0]]), [4.0])[0] == pytest.approx(1.0, abs=1e-14)
+
+
+# ----------------------------------------------------------------------------- Theorem 1 (NEXT-4)
+def test_theorem1_counterexample_conditions_fail_and_conclusion_fails():
+    """§4.1 (P L195-228): condition 1 fails (upto = 0), and indeed pPCA's first vector (e2) is farther from e1
+    than the priming's first vector — the theorem's conclusion needs its conditions (the check is not vacuous)."""
+    X = np.array([[3, 0, 0], [-3, 0, 0], [0, 2, 0], [0, -2, 0], [0, 0, 1], [0, 0, -1]], dtype=float)
+    eps = 0.01
+    V = np.array([[eps, 0, math.sqrt(1 - eps ** 2)], [0, 1, 0]])
+    lam, T = O.truth(X)
+    upto, a_prim, a_ppca, holds = O.theorem1_check(X, V, T, 2, tol=1e-8)
+    assert upto == 0 and holds                       # vacuously true on an empty run …
+    assert a_ppca[0] > a_prim[0]                     # … and the conclusion indeed fails without condition 1
+
+
+def test_theorem1_holds_whenever_conditions_hold():
+    """Near-converged primings (V = T + δ·noise, the regime Theorem 1 describes): conditions hold on a run and
+    the pPCA angles never exceed the priming's there; larger δ shortens the run."""
+    rng = np.random.default_rng(4)
+    n, d, k, l = 800, 30, 6, 4
+    lam = np.exp(-np.arange(1, d + 1) / 3.0)
+    Q = np.linalg.qr(rng.standard_normal((d, d)))[0]
+    X = rng.standard_normal((n, d)) * np.sqrt(lam) @ Q.T
+    X -= X.mean(axis=0)
+    _, T = O.truth(X)
+    runs = []
+    for delta in [1e-4, 1e-3, 1e-2, 5e-2]:
+        for seed in range(3):
+            noise = np.random.default_rng(seed).standard_normal((k + l, d))
+            V = np.vstack([T[: k + l]]) + delta * noise
+            upto, a_prim, a_ppca, holds = O.theorem1_check(X, V, T, k, tol=1e-6)
+            assert holds, (delta, seed, upto)
+            runs.append(upto)
+            if upto == k:
+                lp = [O.lces(a_prim, v) for v in O.PI_THRESHOLDS]
+                lq = [O.lces(a_ppca, v) for v in O.PI_THRESHOLDS]
+                assert all(q >= p for p, q in zip(lp, lq))
+    assert runs[0] == k                              # the smallest perturbation: all k conditions hold

@@ -1,6 +1,9 @@
 """the paper's small-scale synthetic experiment (§5.1, Tables 1/2
 L329-358 / L449-499) on the GPU with the library's own kernels — step counts to an eigenvector streak of 16,
-not seconds (the claim reproduced is the ORDERING: Oja > +pPCA > +pPCA₂ ≈ +pPCA₄).
+not seconds (the claim reproduced is the ORDERING: priming > +pPCA > +pPCA₂ ≈ +pPCA₄ for Oja and EigenGame,
+and little change for the power method).  All three row groups of the tables: Oja, EigenGame
+(α-EigenGame, ppca_prime_eigengame; lr grid the paper's {1 … 1e-6} /1000 for the unnormalised M_b, R11) and
+the power method (block power with the stop rule ε ∈ {1e-3 … 1e-7}, P L362).
 
 Data: 5000 points in 50 dimensions, spectrum 1000 → 1 decaying exponentially (resp. linearly), Gaussian with
 population covariance Q·diag(λ)·Qᵀ (Q Haar), centred, stored fp32; batch 1000 (5 steps per epoch).
@@ -42,17 +45,19 @@ def truth(x: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(u[:, ::-1][:, :K].T, dtype=np.float32)
 
 
-def run(ctx, xm, T, lr, l, steps, seed, want_raw, want_refine=True):
-    """first step (1-based) reaching LCES = K at each V, for the raw Oja vectors and for pPCA_l; angle sum"""
+def run(ctx, xm, T, lr, l, steps, seed, want_raw, want_refine=True, method="oja"):
+    """first step (1-based) reaching LCES = K at each V, for the raw primed vectors (Oja or EigenGame) and for
+    pPCA_l; angle sum"""
     m = K + l
+    prime = P.ppca_prime_oja if method == "oja" else P.ppca_prime_eigengame
     W = torch.empty((m, D), dtype=torch.float32, device="cuda")
     vel = torch.zeros_like(W)
     E = torch.empty((K, D), dtype=torch.float32, device="cuda")
-    step = P.ppca_prime_oja(ctx, xm, m, BATCH, lr, 0.9, 0, 7000 + seed, W, vel, 0)
+    step = prime(ctx, xm, m, BATCH, lr, 0.9, 0, 7000 + seed, W, vel, 0)
     first_raw, first_pp, angsum = [None] * len(VS), [None] * len(VS), 0.0
     for t in range(1, steps + 1):
         try:
-            step = P.ppca_prime_oja(ctx, xm, m, BATCH, lr, 0.9, 1, 0, W, vel, step)
+            step = prime(ctx, xm, m, BATCH, lr, 0.9, 1, 0, W, vel, step)
         except P.PPCAError:
             return first_raw, first_pp, float("inf")
         if want_raw:
@@ -78,6 +83,34 @@ def run(ctx, xm, T, lr, l, steps, seed, want_raw, want_refine=True):
     return first_raw, first_pp, angsum
 
 
+def run_power(ctx, xm, T, eps, l, iters, seed):
+    """Block power priming on m = K + l vectors with the paper's stop rule (P L61-62, ε): first iteration
+    (1-based) reaching LCES = K for the raw columns and for pPCA_l (refine after every iteration); None if the
+    method stopped (all column moves < ε) or ran out of iterations first."""
+    m = K + l
+    W = torch.empty((m, D), dtype=torch.float32, device="cuda")
+    E = torch.empty((K, D), dtype=torch.float32, device="cuda")
+    P.ppca_prime_power(ctx, xm, m, 0, 7000 + seed, W)
+    first_raw, first_pp = [None] * len(VS), [None] * len(VS)
+    for t in range(1, iters + 1):
+        Wp = W.clone()
+        P.ppca_prime_power(ctx, xm, m, 1, 0, W)
+        dots = (W * Wp).sum(dim=1).abs().clamp(max=1.0)
+        moved = float(torch.sqrt(torch.clamp(2 - 2 * dots, min=0)).max())
+        _, lc = P.ppca_eval(ctx, W[:K].contiguous(), T, K, D, VS)
+        for i, c in enumerate(lc):
+            if first_raw[i] is None and c >= K:
+                first_raw[i] = t
+        P.ppca_refine_ex(ctx, xm, W, m, K, E, P.PPCA_REFINE_ORTHONORMAL)
+        _, lc = P.ppca_eval(ctx, E, T, K, D, VS)
+        for i, c in enumerate(lc):
+            if first_pp[i] is None and c >= K:
+                first_pp[i] = t
+        if moved < eps or (all(f is not None for f in first_raw) and all(f is not None for f in first_pp)):
+            break
+    return first_raw, first_pp
+
+
 def summary(vals):
     ok = [v for v in vals if v is not None]
     if len(ok) < len(vals):
@@ -92,6 +125,9 @@ def main():
     # the paper's grid {1e-3, …, 1e-6} (L361) is for a batch-MEAN gradient; ours is the batch sum (R8), so the
     # same steps are 1/1000 of it
     ap.add_argument("--lrs", default="1e-6,1e-7,1e-8,1e-9")
+    ap.add_argument("--eg-lrs", default="1e-3,1e-4,1e-5,1e-6,1e-7,1e-8,1e-9")
+    ap.add_argument("--eg-steps", type=int, default=1500)
+    ap.add_argument("--methods", default="oja,eigengame,power")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     ctx = P.ppca_ctx_create(0, torch.cuda.current_stream())
@@ -106,40 +142,67 @@ def main():
             xd[:, :D] = torch.from_numpy(x)
             xd = xd.cuda()
             data.append((xd, P.matrix(xd, d=D), torch.from_numpy(truth(x)).cuda()))
-        # learning-rate protocol (L361): Oja alone, smallest angular error summed over runs/steps/components
-        best, best_lr = float("inf"), None
-        for lr in [float(v) for v in a.lrs.split(",")]:
-            tot = 0.0
-            for s, (_, xm, T) in enumerate(data):
-                _, _, ang = run(ctx, xm, T, lr, 0, min(a.steps, 200), s, True, want_refine=False)
-                tot += ang
-            lines.append(f"{kind}: lr {lr:g}: summed angle over runs, 200 steps, components = {tot:.4g}")
-            if tot < best:
-                best, best_lr = tot, lr
-        lines.append(f"{kind}: selected lr = {best_lr:g}")
-        res = {}
-        for l in [0, 2, 4]:
-            raws, pps = [], []
-            for s, (_, xm, T) in enumerate(data):
-                fr, fp, _ = run(ctx, xm, T, best_lr, l, a.steps, s, l == 0)
-                raws.append(fr)
-                pps.append(fp)
-            if l == 0:
-                res["oja"] = raws
-            res[f"ppca{l}"] = pps
-        for i, v in enumerate(VS):
-            lines.append(f"{kind}  V=pi/{round(math.pi / v)}:")
-            for name in ["oja", "ppca0", "ppca2", "ppca4"]:
-                label = {"oja": "Oja", "ppca0": "  + pPCA", "ppca2": "  + pPCA_2", "ppca4": "  + pPCA_4"}[name]
-                lines.append(f"   {label:12s} {summary([r[i] for r in res[name]])}")
-            # the orderings
-            oja = [r[i] for r in res["oja"]]
-            p0 = [r[i] for r in res["ppca0"]]
-            wins = sum(1 for o, q in zip(oja, p0) if q is not None and (o is None or q < o))
-            med = lambda xs: np.median([x if x is not None else 10 ** 9 for x in xs])
-            verdicts.append(f"{kind} V=pi/{round(math.pi / v)}: pPCA before Oja in {wins}/{len(oja)} seeds; "
-                            f"median steps Oja {med(oja):.0f}, pPCA {med(p0):.0f}, pPCA_2 {med([r[i] for r in res['ppca2']]):.0f}, "
-                            f"pPCA_4 {med([r[i] for r in res['ppca4']]):.0f}")
+        for method in [x for x in a.methods.split(",") if x in ("oja", "eigengame")]:
+            mname = {"oja": "Oja", "eigengame": "EigenGame"}[method]
+            lrs = a.lrs if method == "oja" else a.eg_lrs
+            nsteps = a.steps if method == "oja" else a.eg_steps
+            # learning-rate protocol (L361): the priming alone, smallest angular error summed over
+            # runs/steps/components
+            best, best_lr = float("inf"), None
+            for lr in [float(v) for v in lrs.split(",")]:
+                tot = 0.0
+                for s, (_, xm, T) in enumerate(data):
+                    _, _, ang = run(ctx, xm, T, lr, 0, min(nsteps, 200), s, True, want_refine=False, method=method)
+                    tot += ang
+                lines.append(f"{kind} {mname}: lr {lr:g}: summed angle over runs, 200 steps, components = {tot:.4g}")
+                if tot < best:
+                    best, best_lr = tot, lr
+            lines.append(f"{kind} {mname}: selected lr = {best_lr:g}")
+            res = {}
+            for l in [0, 2, 4]:
+                raws, pps = [], []
+                for s, (_, xm, T) in enumerate(data):
+                    fr, fp, _ = run(ctx, xm, T, best_lr, l, nsteps, s, l == 0, method=method)
+                    raws.append(fr)
+                    pps.append(fp)
+                if l == 0:
+                    res["raw"] = raws
+                res[f"ppca{l}"] = pps
+            for i, v in enumerate(VS):
+                lines.append(f"{kind}  V=pi/{round(math.pi / v)}:")
+                for name in ["raw", "ppca0", "ppca2", "ppca4"]:
+                    label = {"raw": mname, "ppca0": "  + pPCA", "ppca2": "  + pPCA_2", "ppca4": "  + pPCA_4"}[name]
+                    lines.append(f"   {label:12s} {summary([r[i] for r in res[name]])}")
+                # the orderings
+                raw = [r[i] for r in res["raw"]]
+                p0 = [r[i] for r in res["ppca0"]]
+                wins = sum(1 for o, q in zip(raw, p0) if q is not None and (o is None or q < o))
+                med = lambda xs: np.median([x if x is not None else 10 ** 9 for x in xs])
+                verdicts.append(f"{kind} V=pi/{round(math.pi / v)}: pPCA before {mname} in {wins}/{len(raw)} seeds; "
+                                f"median steps {mname} {med(raw):.0f}, pPCA {med(p0):.0f}, "
+                                f"pPCA_2 {med([r[i] for r in res['ppca2']]):.0f}, pPCA_4 {med([r[i] for r in res['ppca4']]):.0f}")
+        if "power" in a.methods:
+            # the paper's protocol (L362): termination conditions ε ∈ {1e-3 … 1e-7}, the best ε, pPCA on top;
+            # steps = power iterations (each one pass over the 5000 rows = 5 minibatch steps of 1000)
+            best_eps, best_key = None, None
+            table = {}
+            for eps in [1e-3, 1e-4, 1e-5, 1e-6, 1e-7]:
+                runs = [run_power(ctx, xm, T, eps, 0, 400, s) for s, (_, xm, T) in enumerate(data)]
+                table[eps] = runs
+                key = sum(r[0][0] if r[0][0] is not None else 10 ** 6 for r in runs)
+                if best_key is None or key < best_key:
+                    best_key, best_eps = key, eps
+            lines.append(f"{kind} Power: selected eps = {best_eps:g} (fewest iterations to the π/8 streak)")
+            runs = table[best_eps]
+            for i, v in enumerate(VS):
+                lines.append(f"{kind}  V=pi/{round(math.pi / v)} (power iterations):")
+                lines.append(f"   {'Power':12s} {summary([r[0][i] for r in runs])}")
+                lines.append(f"   {'  + pPCA':12s} {summary([r[1][i] for r in runs])}")
+                raw = [r[0][i] for r in runs]
+                pp = [r[1][i] for r in runs]
+                same = sum(1 for o, q in zip(raw, pp) if q is not None and (o is None or q <= o))
+                verdicts.append(f"{kind} V=pi/{round(math.pi / v)}: power + pPCA at or before power in {same}/{len(raw)} "
+                                f"seeds (the paper: little gain for the power method, L363)")
     lines.append("# orderings")
     lines += verdicts
     txt = "\n".join(lines)
