@@ -184,12 +184,12 @@ def time_to_subspace_target(P, ctx, Xm, w, s, dev, stream, max_over_ranks, targe
     import torch
     k1 = w.k + 1
     Wr = torch.empty((w.m, s.d), dtype=torch.float32, device=dev)
-    # the reference: 60 tensor-core iterations, then 12 on the exact-fp32 CUDA-core pass (its span is not held
+    # the reference: 60 tensor-core iterations, then 16 on the exact-fp32 CUDA-core pass (its span is not held
     # back by the bf16 rounding of Y in product 2, R27) and a CUDA-core refine
     P.ppca_prime_power(ctx, Xm, w.m, 60, w.init_seed + 7919, Wr)
     P.ppca_set_pass_impl(ctx, 1)
     try:
-        P.ppca_prime_power(ctx, Xm, w.m, 12, 0, Wr)
+        P.ppca_prime_power(ctx, Xm, w.m, 16, 0, Wr)
         Eref = torch.empty((k1, s.d), dtype=torch.float32, device=dev)
         th_ref, _ = P.ppca_refine(ctx, Xm, Wr, w.m, k1, Eref)
     finally:
@@ -207,21 +207,24 @@ def time_to_subspace_target(P, ctx, Xm, w, s, dev, stream, max_over_ranks, targe
     W2 = torch.empty_like(Wr)
     E = torch.empty((w.k, s.d), dtype=torch.float32, device=dev)
     P.ppca_prime_power(ctx, Xm, w.m, 0, w.init_seed, W2)
-    reached, errs = None, []
+    reached, measured, errs = None, None, []
     for t in range(1, w.iters + 1):
         P.ppca_prime_power(ctx, Xm, w.m, 1, 0, W2)
-        P.ppca_refine(ctx, Xm, W2, w.m, w.k, E)
+        P.ppca_refine_ex(ctx, Xm, W2, w.m, w.k, E, P.PPCA_REFINE_ORTHONORMAL)
         errs.append(sub_err(E))
-        if errs[-1] <= target:
+        if measured is None and errs[-1] <= target:
+            measured = t
+        if errs[-1] + bound <= target:                # certified: the error to the TRUE subspace is ≤ target
             reached = t
             break
-    out = {"target": f"top-{w.k} subspace error <= {target} vs a residual-certified reference",
-           "iterations": reached, "subspace_error_per_iteration": errs,
-           "reference": {"iterations": "60 tensor-core + 12 exact-fp32", "theta_1": float(th_ref[0]),
+    out = {"target": f"top-{w.k} subspace error <= {target} to the true subspace (measured error vs the reference "
+                     f"+ the reference's certified bound)",
+           "iterations": reached, "iterations_measured_only": measured, "subspace_error_per_iteration": errs,
+           "reference": {"iterations": "60 tensor-core + 16 exact-fp32", "theta_1": float(th_ref[0]),
                          "max_residual_over_theta1":
                          float(np.max(res[: w.k]) / th_ref[0]), "certified_subspace_bound": bound,
                          "how": "power + refine from an independent start; ppca_ritz_residuals (exact-fp32 pass)"}}
-    out["certified"] = bool(reached and errs[-1] + bound <= target)   # measured error + reference bound
+    out["certified"] = reached is not None
     if reached:
         def nob():
             pass

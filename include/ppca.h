@@ -267,6 +267,12 @@ ppca_status ppca_get_kernel_time(ppca_ctx* ctx, int which, double* ms_total, int
  * with the power pass as two kernels instead of the single-read fused kernel; 3 reports as 2).
  * Returns UNSUPPORTED if the requested path cannot run this matrix. */
 ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);
+/* Re-orthonormalisation of the power iteration: 0 = auto — with world > 1 and d·m² ≥ 2^28 (C5)
+ * the CholQR is split by d-slices (reduce-scatter of Z, slice Gram, m×m all-reduce, slice apply, all-gather of
+ * W) so the d·m² work per rank drops by the rank count; 1 = replicated on every rank; -1 = the split path over
+ * the context's ranks even at world 1 (needs a communicator; tests); b ≥ 2 at world 1 = b emulated slices
+ * without NCCL (tests).  The result is the same CholQR (the Gram summed in another order). */
+ppca_status ppca_set_orth_split(ppca_ctx* ctx, int split);
 /* Implementation used by the most recent pass (1 = SIMT, 2 = tcgen05; 0 = none yet). */
 int ppca_last_pass_impl(const ppca_ctx* ctx);
 

@@ -32,7 +32,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
            "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
            "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals", "ppca_refine_ex",
-           "ppca_check_theorem1"]
+           "ppca_check_theorem1", "ppca_set_orth_split"]
 
 
 class PPCAError(RuntimeError):
@@ -79,6 +79,7 @@ def load(path: str = LIB_PATH):
         "ppca_generate": (I, [P, ctypes.POINTER(ppca_gen_spec), P, I64, ctypes.POINTER(I64), P]),
         "ppca_prime_power": (I, [P, ctypes.POINTER(ppca_matrix), I, I, D, ctypes.c_uint64, P, P, ctypes.POINTER(I)]),
         "ppca_collective_count": (I64, [P]),
+        "ppca_set_orth_split": (I, [P, I]),
         "ppca_ritz_residuals": (I, [P, ctypes.POINTER(ppca_matrix), P, I, P, P, P]),
         "ppca_check_theorem1": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, P, D, ctypes.POINTER(I), P, P,
                                     ctypes.POINTER(I)]),
@@ -236,6 +237,10 @@ def ppca_ctx_destroy(ctx) -> None:
 
 def ppca_launch_count(ctx) -> int:
     return int(load().ppca_launch_count(ctx))
+
+
+def ppca_set_orth_split(ctx, split: int) -> None:
+    _check(ctx, load().ppca_set_orth_split(ctx, split), "ppca_set_orth_split")
 
 
 def ppca_collective_count(ctx) -> int:

@@ -34,6 +34,8 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 static NcclApi g_nccl;
 
@@ -51,6 +53,8 @@ static bool nccl_load() {
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
   g_nccl.CommGetAsyncError = (decltype(g_nccl.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
   g_nccl.CommCount = (decltype(g_nccl.CommCount))dlsym(h, "ncclCommCount");
+  g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
   g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
   return g_nccl.loaded;
 }
@@ -145,6 +149,91 @@ ppca_status allreduce_zs(Ctx* c, float* Z, size_t nz, double* S, size_t ns) {
   if (r != ncclSuccess || r2 != ncclSuccess)
     return set_error(c, PPCA_ERR_NCCL, "grouped ncclAllReduce [Z|S]: %s", g_nccl.GetErrorString(r != ncclSuccess ? r : r2));
   c->collectives++;
+  return PPCA_OK;
+}
+
+// ----------------------------------------------------------------------------- distributed CholQR (§6)
+// The replicated part of a power iteration is W ← orth(Z) on the full d×m Z (d·m² fp64 MAC in the Gram, d·m²/2
+// in the apply) on every rank.  Split by d-slices instead: the pass writes Z d-blocked [G][m][ds] (ds = d/G,
+// launch_reduce_zp), one grouped NCCL operation reduce-scatters the slices (rank g receives Σ_ranks Z[:, slice g])
+// and all-reduces S; every rank forms its slice's Gram, the m×m Grams are all-reduced, every rank factors the
+// same G = Σ_g G_g (Cholesky + L⁻¹, replicated, m×m), applies L⁻¹ to its slice, and an all-gather assembles W.
+// Exchange volume equals the all-reduce's (reduce-scatter + all-gather), plus one m×m all-reduce; the d·m² work
+// per rank drops by G.  Test modes on one GPU: split = -1 runs the NCCL path with world's ranks (one-rank
+// communicator), split = b ≥ 2 emulates b slices without NCCL (the blocked layout and slice arithmetic).
+static int orth_blocks(const Ctx* c, int m, int64_t d, int impl) {
+  if (impl != 2) return 0;                                 // the SIMT pass writes Z plain
+  if (c->orth_split == 1) return 0;
+  if (c->orth_split == -1) return (c->nccl_comm && d % (4 * c->world) == 0) ? c->world : 0;
+  if (c->orth_split >= 2) return (c->world == 1 && d % (4 * c->orth_split) == 0) ? c->orth_split : 0;
+  const bool big = (double)d * m * m >= (double)(1 << 28);     // C5: 2^30; C3, C4: ≤ 2^24 (NCCL latency wins there)
+  return (c->world > 1 && c->nccl_comm && big && d % (4 * c->world) == 0) ? c->world : 0;
+}
+
+__global__ void add_into_f64_kernel(double* __restrict__ acc, const double* __restrict__ v, int64_t count) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < count) acc[e] += v[e];
+}
+
+// W[i][g·ds + x] = Wb[(g·m + i)·ds + x]
+__global__ void unblock_kernel(const float* __restrict__ Wb, int m, int64_t ds, int blocks, float* __restrict__ W) {
+  const int64_t d = ds * blocks;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (e >= (int64_t)m * d) return;
+  const int64_t i = e / d, col = e % d, g = col / ds, x = col % ds;   // ds % 4 == 0: a float4 stays in one block
+  *reinterpret_cast<float4*>(W + e) = *reinterpret_cast<const float4*>(Wb + (g * m + i) * ds + x);
+}
+
+// the exchange of the distributed mode: reduce-scatter of the d-blocked Z + all-reduce of S, one group
+static ppca_status exchange_dist(Ctx* c, const float* Zb, float* Zg, size_t slice, double* S, size_t ns) {
+  ncclResult_t r = g_nccl.GroupStart();
+  if (r == ncclSuccess)
+    r = g_nccl.ReduceScatter(Zb, Zg, slice, ncclFloat32, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
+  if (r == ncclSuccess && ns) r = g_nccl.AllReduce(S, S, ns, ncclFloat64, ncclSum, (ncclComm_t)c->nccl_comm, c->stream);
+  ncclResult_t r2 = g_nccl.GroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return set_error(c, PPCA_ERR_NCCL, "reduce-scatter Z / all-reduce S: %s", g_nccl.GetErrorString(r != ncclSuccess ? r : r2));
+  c->collectives++;
+  return PPCA_OK;
+}
+
+// W ← orth(Z) from the d-blocked Z (after exchange_dist when NCCL runs it).  One CholQR pass, fp64 Gram / factor /
+// apply as in cholqr(); the Gram is the sum of the slice Grams (a fixed order: slices 0..G-1 in the emulation,
+// NCCL's reduction order across ranks).
+static ppca_status cholqr_dist(Ctx* c, float* Zb, const float* Zg, float* W, int m, int64_t d, int blocks) {
+  const int64_t ds = d / blocks;
+  const bool nccl = c->orth_split <= 0;                    // the real path (NCCL); otherwise the emulation
+  double* G = (double*)scratch(c, S_GRAM, (size_t)2 * m * m * sizeof(double));
+  double* Linv = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64);
+  float* Wb = (float*)scratch(c, S_W2, (size_t)m * d * sizeof(float));
+  float* Wg = (float*)scratch(c, S_DIST, (size_t)2 * m * ds * sizeof(float)) + (size_t)m * ds;
+  if (!G || !Linv || !Wb || !Wg) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  int* row_map = (int*)(Linv + (size_t)m * m);
+  int* m_out = row_map + m;
+  if (nccl) {
+    PPCA_TRY(vec_gram(c, Zg, m, ds, G));
+    PPCA_TRY(allreduce(c, G, (size_t)m * m, true));
+  } else {
+    for (int g = 0; g < blocks; ++g) {
+      PPCA_TRY(vec_gram(c, Zb + (size_t)g * m * ds, m, ds, g ? G + (size_t)m * m : G));
+      if (g) {
+        add_into_f64_kernel<<<(unsigned)ceil_div((int64_t)m * m, 256), 256, 0, c->stream>>>(G, G + (size_t)m * m, (int64_t)m * m);
+        PPCA_LAUNCH_CHECK(c, "add_into_f64");
+      }
+    }
+  }
+  PPCA_TRY(chol_inv_on(c, G, m, Linv, row_map, m_out, c->stream));
+  if (nccl) {
+    PPCA_TRY(apply_lower_on(c, Linv, m, Zg, ds, Wg, c->stream));
+    ncclResult_t r = g_nccl.AllGather(Wg, Wb, (size_t)m * ds, ncclFloat32, (ncclComm_t)c->nccl_comm, c->stream);
+    if (r != ncclSuccess) return set_error(c, PPCA_ERR_NCCL, "all-gather W: %s", g_nccl.GetErrorString(r));
+    c->collectives++;
+  } else {
+    for (int g = 0; g < blocks; ++g)
+      PPCA_TRY(apply_lower_on(c, Linv, m, Zb + (size_t)g * m * ds, ds, Wb + (size_t)g * m * ds, c->stream));
+  }
+  unblock_kernel<<<(unsigned)ceil_div((int64_t)m * d, 1024), 256, 0, c->stream>>>(Wb, m, ds, blocks, W);
+  PPCA_LAUNCH_CHECK(c, "unblock");
   return PPCA_OK;
 }
 
@@ -309,6 +398,12 @@ ppca_status ppca_last_error(const ppca_ctx* h, char* msg, size_t cap) {
 int64_t ppca_launch_count(const ppca_ctx* h) { return h ? h->c.launches : -1; }
 int64_t ppca_collective_count(const ppca_ctx* h) { return h ? h->c.collectives : -1; }
 
+ppca_status ppca_set_orth_split(ppca_ctx* h, int split) {
+  if (!h || split < -1 || split > 64) return PPCA_ERR_INVALID_ARG;
+  h->c.orth_split = split;
+  return PPCA_OK;
+}
+
 int ppca_experiments_enabled(void) {
 #ifdef PPCA_EXPERIMENTS
   return 1;
@@ -403,8 +498,14 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     PPCA_TRY(check_cuda(c, cudaMemsetAsync(theta_dev, 0, (size_t)iters * m * sizeof(double), c->stream), "zero theta"));
   PassPlan plan;
   PPCA_TRY(pass_prepare(c, X, m, &plan));
+  const int oblk = orth_blocks(c, m, d, plan.impl);        // > 0: the distributed CholQR (§6)
+  float* Zg = nullptr;
+  if (oblk > 0) {
+    Zg = (float*)scratch(c, S_DIST, (size_t)2 * m * (d / oblk) * sizeof(float));
+    if (!Zg) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  }
   // pre-touch the scratch the loop uses so no allocation happens while the side stream is busy
-  if (!scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double)) || !scratch(c, S_GRAM, (size_t)m * m * sizeof(double)) ||
+  if (!scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double)) || !scratch(c, S_GRAM, (size_t)2 * m * m * sizeof(double)) ||
       !scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64) ||
       !scratch(c, S_W2, (size_t)m * d * sizeof(float)) || !scratch(c, S_SIDE_PART, vec_gram_part_bytes(c, m, d)))
     return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
@@ -433,7 +534,9 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       cudaStreamWaitEvent(c->stream, ev_side[t & 1], 0);   // Ritz t-2 done with S, Bm
       cudaStreamWaitEvent(c->stream, ev_gram, 0);          // the side Gram of W'_{t-1} read it before prep_w rewrites
     }
+    c->z_block_cols = oblk > 0 ? d / oblk : 0;               // the pass writes Z d-blocked for the slices
     st = pass_power(c, X, &plan, W, m, Z, S);               // Z = YᵀX, S = YᵀY  (local)
+    c->z_block_cols = 0;
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
       // side stream, once the pass is done (a Gram overlapping the persistent pass would take its SMs): Bm =
@@ -447,7 +550,10 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       st = pass_reduce_deferred_s(c, S, c->side);
       if (st != PPCA_OK) break;
     }
-    st = allreduce_zs(c, Z, (size_t)m * d, S, (size_t)m * m);   // the only collective: [Z | S], one group
+    if (oblk > 0 && c->orth_split <= 0)
+      st = exchange_dist(c, Z, Zg, (size_t)m * (d / oblk), S, (size_t)m * m);   // slices of Z + S, one group
+    else if (oblk == 0)
+      st = allreduce_zs(c, Z, (size_t)m * d, S, (size_t)m * m);   // the only collective: [Z | S], one group
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
       cudaEventRecord(ev_main[t & 1], c->stream);
@@ -465,7 +571,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
                       "keep W_t");
       if (st != PPCA_OK) break;
     }
-    st = cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
+    st = oblk > 0 ? cholqr_dist(c, Z, Zg, W, m, d, oblk) : cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
     if (st != PPCA_OK) break;
     done = t + 1;
     if (stop_rule) {                                 // P L61-62: stop once every column moved less than eps

@@ -54,6 +54,9 @@ struct Ctx {
   int sm_count = 148;
   int64_t launches = 0;
   int64_t collectives = 0;            // NCCL operations enqueued (bench evidence of the exchange)
+  // distributed CholQR (§6): 0 = auto, 1 = replicated, b ≥ 2 = d-slices (world == 1: b emulated slices, tests)
+  int orth_split = 0;
+  int64_t z_block_cols = 0;           // > 0: the pass writes Z d-blocked [d/z_block_cols][m][z_block_cols]
   // pass timing (bench): event pairs recorded around each pass
   bool timing = false;
   std::vector<cudaEvent_t> tev;
@@ -89,6 +92,7 @@ enum Slot {
   S_P3,                            // Prop. 3 checker workspace (fp64)
   S_P3F,                           // Prop. 3 checker stacked vectors [B; T] (fp32)
   S_EPS,                           // power stop rule: W_t copy + column dots
+  S_DIST,                          // distributed CholQR: this rank's Z slice and W slice
 };
 
 void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory

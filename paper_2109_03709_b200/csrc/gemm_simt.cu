@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256) tn_kernel(const TA* __restrict__ A, int64
   __shared__ float As[TN_BK][TN_BM + 4];
   __shared__ float Bs[TN_BK][TN_BN + 4];
   const int tid = threadIdx.x;
-  const int64_t m0 = (int64_t)blockIdx.x * TN_BM;
-  const int64_t n0 = (int64_t)blockIdx.y * TN_BN;
+  const int64_t m0 = (int64_t)blockIdx.y * TN_BM;      // M ≤ 128 (vectors): the y dimension
+  const int64_t n0 = (int64_t)blockIdx.x * TN_BN;      // N = d can exceed 65535 tiles (huge d): x
   const int64_t kbeg = (int64_t)blockIdx.z * rows_per_split;
   const int64_t kend = min(K, kbeg + rows_per_split);
   const int tx = tid % 16, ty = tid / 16;    // tx → N (8 each), ty → M (4 each)
@@ -240,7 +240,8 @@ ppca_status launch_tn_splitk(Ctx* c, const TA* A, int64_t lda, const TB* B, int6
                              double* P, int64_t M, int64_t N, int64_t K, int nsplit) {
   if (M <= 0 || N <= 0) return PPCA_OK;
   int64_t rps = ceil_div(ceil_div(K > 0 ? K : 1, nsplit), TN_BK) * TN_BK;
-  dim3 grid((unsigned)ceil_div(M, TN_BM), (unsigned)ceil_div(N, TN_BN), (unsigned)nsplit);
+  if (ceil_div(M, TN_BM) > 65535) return set_error(c, PPCA_ERR_UNSUPPORTED, "tn_kernel: M = %lld", (long long)M);
+  dim3 grid((unsigned)ceil_div(N, TN_BN), (unsigned)ceil_div(M, TN_BM), (unsigned)nsplit);
   bool vecB = (ldb * sizeof(TB)) % 16 == 0 && ((uintptr_t)B % 16) == 0;
   tn_kernel<TA, TB><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, P, M, N, K, rps, false, vecB);
   PPCA_LAUNCH_CHECK(c, "tn_kernel");

@@ -174,8 +174,14 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
 // 8 warps split the partials; this one serves the short windows of the minibatch steps, nrg ≤ 16)
 // Z[j][x] = Σ_g Zp[g][x][j]: block (x, 32 consecutive j), warp w sums g ≡ w (mod 8) (8 loads in flight),
 // the 8 warp sums are added in warp order.
+// Z's layout: plain [m][d] (ds = d) or d-blocked [d/ds][m][ds] (the slices of the distributed CholQR, §6):
+// element (j, x) lives at ((x / ds)·m + j)·ds + x % ds
+__device__ __forceinline__ int64_t z_index(int j, int64_t x, int m, int64_t ds) {
+  return ((x / ds) * m + j) * ds + x % ds;
+}
+
 __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
-                                                             int mp, int m, int64_t d, float* __restrict__ Z) {
+                                                             int mp, int m, int64_t d, float* __restrict__ Z, int64_t ds) {
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t x = blockIdx.x;
@@ -188,52 +194,57 @@ __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __rest
   if (warp == 0 && j < m) {
     double t = 0.0;
     for (int w = 0; w < 8; ++w) t += part[w][lane];
-    Z[(int64_t)j * d + x] = (float)t;
+    Z[z_index(j, x, m, ds)] = (float)t;
   }
 }
 
-static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z);
-
-constexpr int ZP_XB = 8;
+// ZP_XB columns × all mp features per block (≤ 16 elements per thread), the partials of 4 row groups in flight;
+// the sums leave through shared memory as ZP_XB-float (128-byte) runs of Z's rows
+constexpr int ZP_XB = 32;
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
-                                                        int m, int64_t d, float* __restrict__ Z) {
+                                                        int m, int64_t d, float* __restrict__ Z, int64_t ds) {
   __shared__ float tr[128][ZP_XB + 1];
   const int64_t x0 = (int64_t)blockIdx.x * ZP_XB;
-  const int cnt = ZP_XB * mp;                        // ≤ 1024: ≤ 4 elements per thread
+  const int cnt = ZP_XB * mp;                        // ≤ 4096: ≤ 16 elements per thread
+  const int64_t xrem = (d - x0) * mp;                // elements of the block inside [0, d)
   const float* base = Zp + x0 * mp;
   const int64_t gstride = dpad * mp;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t g0 = 0; g0 < nrg; g0 += 8) {
-    float v[8][4];
+  double acc[16];
 #pragma unroll
-    for (int gg = 0; gg < 8; ++gg)
+  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+  for (int64_t g0 = 0; g0 < nrg; g0 += 4) {
+    float v[4][16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+    for (int gg = 0; gg < 4; ++gg)
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
         const int e = threadIdx.x + 256 * u;
-        v[gg][u] = (g0 + gg < nrg && e < cnt) ? base[(g0 + gg) * gstride + e] : 0.f;
+        v[gg][u] = (g0 + gg < nrg && e < cnt && e < xrem) ? base[(g0 + gg) * gstride + e] : 0.f;
       }
 #pragma unroll
-    for (int gg = 0; gg < 8; ++gg)
+    for (int gg = 0; gg < 4; ++gg)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += (double)v[gg][u];
+      for (int u = 0; u < 16; ++u) acc[u] += (double)v[gg][u];
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 16; ++u) {
     const int e = threadIdx.x + 256 * u;
     if (e < cnt) tr[e % mp][e / mp] = (float)acc[u];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < m * ZP_XB; e += 256) {
     const int j = e / ZP_XB, xl = e % ZP_XB;
-    if (x0 + xl < d) Z[(int64_t)j * d + x0 + xl] = tr[j][xl];
+    if (x0 + xl < d) Z[z_index(j, x0 + xl, m, ds)] = tr[j][xl];
   }
 }
 
 static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z) {
+  const int64_t ds = c->z_block_cols > 0 ? c->z_block_cols : d;
   if (nrg > 16)
-    reduce_zp_cols_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+    reduce_zp_cols_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z,
+                                                                                            ds);
   else
-    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z);
+    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z, ds);
 }
 
 // ============================================================================ host side
@@ -423,15 +434,6 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   return PPCA_OK;
 }
 
-ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S) {
-  const int mp = pad16(m);
-  __nv_bfloat16* Wb;
-  float* Wr;
-  PPCA_TRY(prep_w(c, W, m, mp, X->d, &Wb, &Wr));
-  const_cast<PassPlan*>(plan)->Wop = Wr;
-  return run_ka(c, X, Wb, m, mp, S, nullptr, 0, 1, nullptr, plan->tiles_dev, plan->ntiles_sel);
-}
-
 // Y of a K-split row window and S = YᵀY in one pass over the partials: block = YS_RB rows.  Y = Σ_parts Ypart
 // in part order (fp32), written as the Yᵀ bf16 pair [Y_hi; Y_lo] [2·mp][ldyt] (rows ≥ n zero) for kernel B;
 // the block's rows also give a partial S_b = Σ_rows y yᵀ (fp64 products and sums, 4×4 register tiles per
@@ -511,16 +513,47 @@ __global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Y
   }
 }
 
+static int pick_ksplit_tiles(const Ctx* c, const ppca_matrix* X, int64_t ntiles, int64_t nk);
+
 // K split for short row windows (a minibatch step): enough (tile, K part) items to cover the SMs
 static int pick_ksplit(const Ctx* c, const ppca_matrix* X, int64_t nk) {
+  return pick_ksplit_tiles(c, X, ceil_div(X->n_local, ka::BM), nk);
+}
+
+static int pick_ksplit_tiles(const Ctx* c, const ppca_matrix* X, int64_t ntiles, int64_t nk) {
   if (X->dtype == PPCA_F32) return 1;                 // the converter kernel A has no K split
-  const int64_t ntiles = ceil_div(X->n_local, ka::BM);
   const int64_t ctas = persistent_ctas(c);
   if (2 * ntiles > ctas) return 1;
   int64_t ks = std::min<int64_t>(nk, std::max<int64_t>(1, ctas / ntiles));
   const int64_t kper = ceil_div(nk, ks);
   return (int)ceil_div(nk, kper);
 }
+
+// refine-mode pass (S only).  Fewer row tiles than SMs (huge d with few rows, a row-tile sample): K split
+// over the SMs, the fp32 partial Y of each K part summed in part order, S from the sum (ysum_s)
+ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, const float* W, int m, double* S) {
+  const int mp = pad16(m);
+  __nv_bfloat16* Wb;
+  float* Wr;
+  PPCA_TRY(prep_w(c, W, m, mp, X->d, &Wb, &Wr));
+  const_cast<PassPlan*>(plan)->Wop = Wr;
+  const int64_t n = X->n_local;
+  const int64_t ntiles = plan->tiles_dev ? plan->ntiles_sel : ceil_div(n, ka::BM);
+  const int ksplit = ntiles > 0 ? pick_ksplit_tiles(c, X, ntiles, ceil_div(X->d, ka::BK)) : 1;
+  if (ksplit == 1) return run_ka(c, X, Wb, m, mp, S, nullptr, 0, 1, nullptr, plan->tiles_dev, plan->ntiles_sel);
+  float* Ypart = (float*)scratch(c, S_TC3, (size_t)ksplit * n * mp * sizeof(float));
+  const int64_t nb = ceil_div(n, (int64_t)YS_RB);
+  double* Sp = (double*)scratch(c, S_NTSTAGE, (size_t)nb * m * m * sizeof(double));
+  if (!Ypart || !Sp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (plan->tiles_dev)                          // rows outside the sample stay zero in every part
+    PPCA_TRY(check_cuda(c, cudaMemsetAsync(Ypart, 0, (size_t)ksplit * n * mp * sizeof(float), c->stream), "zero Y"));
+  PPCA_TRY(run_ka(c, X, Wb, m, mp, S, nullptr, 0, ksplit, Ypart, plan->tiles_dev, plan->ntiles_sel));
+  ysum_s_kernel<<<(unsigned)nb, 256, (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream>>>(Ypart, ksplit, n, mp, m,
+                                                                                            nullptr, 0, Sp);
+  PPCA_LAUNCH_CHECK(c, "ysum_s");
+  return launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S);
+}
+
 
 template <int XM, int NSTA, int NWS, int NSTB>
 static constexpr size_t fused_smem() {

@@ -138,10 +138,101 @@ __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __re
   }
 }
 
+// m in (120, 128] (C5): the 136 upper 8×8 tiles balanced over 4 warps — one per SM sub-partition, equal work:
+// 128 main tiles (the 120 off-diagonal ones and 8 diagonal ones) plus the other 8 diagonal tiles cut into 128
+// 2×2 sub-tiles, one per thread (64 + 4 accumulators; the 5-warp kernel above gave one sub-partition two warps).
+__global__ void __launch_bounds__(128) vec_gram_bal16_kernel(const float* __restrict__ V, int m, int64_t d,
+                                                             int64_t cols_per_split, double* __restrict__ P) {
+  constexpr int MP = 128, LD = MP + 2, PER = MP * GK / 128;
+  __shared__ __align__(16) double sv[GK * LD];
+  const int64_t xb = (int64_t)blockIdx.x * cols_per_split;
+  const int64_t xe = min(d, xb + cols_per_split);
+  const int t = threadIdx.x;
+  int bi, bj;                                      // main tile
+  if (t < 120) {                                   // off-diagonal (bi < bj) in row order
+    int r = 0, u = t;
+    while (u >= 15 - r) { u -= 15 - r; ++r; }
+    bi = r;
+    bj = r + 1 + u;
+  } else {
+    bi = bj = t - 120;                             // diagonal tiles 0..7
+  }
+  const int xt = 8 + (t >> 4), xs = t & 15;        // extra: diagonal tile 8..15, 2×2 sub-tile xs
+  const int xr = xt * 8 + 2 * (xs >> 2), xc = xt * 8 + 2 * (xs & 3);
+  double acc[8][8], ex[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  float nxt[PER];
+  auto fetch = [&](int64_t x0) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = t + 128 * u;
+      const int r = e / GK, cc = e % GK;
+      const int64_t x = x0 + cc;
+      nxt[u] = (r < m && x < xe) ? __ldg(V + (int64_t)r * d + x) : 0.f;
+    }
+  };
+  if (xb < xe) fetch(xb);
+  for (int64_t x0 = xb; x0 < xe; x0 += GK) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = t + 128 * u;
+      sv[(e % GK) * LD + e / GK] = (double)nxt[u];
+    }
+    __syncthreads();
+    if (x0 + GK < xe) fetch(x0 + GK);
+#pragma unroll 2
+    for (int k = 0; k < GK; ++k) {
+      const double* row = sv + k * LD;
+      const double2* pa = reinterpret_cast<const double2*>(row + bi * 8);
+      const double2* pb = reinterpret_cast<const double2*>(row + bj * 8);
+      double a[8], b[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 va = pa[q], vb = pb[q];
+        a[2 * q] = va.x; a[2 * q + 1] = va.y;
+        b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
+      }
+      const double2 ea = *reinterpret_cast<const double2*>(row + xr);
+      const double2 eb = *reinterpret_cast<const double2*>(row + xc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      ex[0][0] = fma(ea.x, eb.x, ex[0][0]);
+      ex[0][1] = fma(ea.x, eb.y, ex[0][1]);
+      ex[1][0] = fma(ea.y, eb.x, ex[1][0]);
+      ex[1][1] = fma(ea.y, eb.y, ex[1][1]);
+    }
+  }
+  double* Pz = P + (int64_t)blockIdx.x * m * m;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gi = bi * 8 + i, gj = bj * 8 + j;
+      if (gi < m && gj < m) {
+        Pz[(int64_t)gi * m + gj] = acc[i][j];
+        Pz[(int64_t)gj * m + gi] = acc[i][j];
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (xr + i < m && xc + j < m) Pz[(int64_t)(xr + i) * m + xc + j] = ex[i][j];   // full diagonal tile
+}
+
 // short d (fewer GK-column stages than SMs, e.g. C3's 32) or m > 128: the 32×32-tile kernel over
 // (tile, tile, split) keeps more CTAs busy (7.4 vs 9.3 µs at d = 1024, m = 64); otherwise the 8×8-register-tile
 // kernel over one d-slab per SM
-static bool gram_short(const Ctx* c, int m, int64_t d) { return m > 128 || ceil_div(d, (int64_t)GK) < c->sm_count; }
+// (and m ≤ 64: the 8×8-tile kernel would leave most of its threads without a tile — 1 of 160 at m = 8)
+static bool gram_short(const Ctx* c, int m, int64_t d) {
+  return m > 128 || m <= 64 || ceil_div(d, (int64_t)GK) < c->sm_count;
+}
 
 static void vec_gram_split(const Ctx* c, int m, int64_t d, int* nsplit_out, int64_t* cps_out) {
   int64_t cps;
@@ -186,7 +277,8 @@ ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cud
   else if (mb <= 6) launch_gram_mb<6>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 8) launch_gram_mb<8>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 12) launch_gram_mb<12>(nsplit, st, V, m, d, cps, P);
-  else if (mb <= 16) launch_gram_mb<16>(nsplit, st, V, m, d, cps, P);
+  else if (mb <= 15) launch_gram_mb<16>(nsplit, st, V, m, d, cps, P);
+  else vec_gram_bal16_kernel<<<nsplit, 128, 0, st>>>(V, m, d, cps, P);
   PPCA_LAUNCH_CHECK(c, "vec_gram");
   return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G, st);
 }
@@ -627,8 +719,16 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
   for (int e = threadIdx.x; e < m_in * (RP - rows); e += 256) ct[(e / (RP - rows)) * LDT + rows + e % (RP - rows)] = 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = lane >> 3, cg = lane & 7;
-  const int i0 = warp * 4 * RPT + rg * RPT;
-  const int jend = lower ? min(m_in, (warp + 1) * 4 * RPT) : m_in;    // warp-uniform
+  // row sets: plain — warp w owns rows [4·RPT·w, 4·RPT·(w+1)); balanced (lower, RPT = 4) — warp w owns the 8-row
+  // blocks w and 15 − w, so every warp (one per SM sub-partition pair) does the same triangular work
+  const bool bal = lower && RPT == 4;
+  int rows_t[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+    rows_t[r] = bal ? (r < 2 ? 8 * warp + 2 * rg + r : 8 * (15 - warp) + 2 * rg + (r - 2)) : warp * 4 * RPT + rg * RPT + r;
+  const int i0 = rows_t[0];
+  const int jend = !lower ? m_in : bal ? min(m_in, 8 * (16 - warp)) : min(m_in, (warp + 1) * 4 * RPT);
+  const int jsplit = bal ? min(jend, 8 * (warp + 1)) : jend;          // below it all RPT rows, above only the high ones
   const int64_t nchunks = (d + AT_COLS - 1) / AT_COLS;
   float nxt[PER];
   auto fetch = [&](int64_t ch) {
@@ -657,15 +757,15 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
 #pragma unroll 4
-    for (int j = 0; j < jend; ++j) {
+    for (int j = 0; j < jsplit; ++j) {
       const float4 b = *reinterpret_cast<const float4*>(ins + j * AT_COLS + cg * 4);
       double a[RPT];
       if constexpr (RPT == 1) {
         a[0] = ct[j * LDT + i0];
       } else {
 #pragma unroll
-        for (int r = 0; r < RPT; r += 2) {        // i0 is even for RPT ≥ 2: 16-byte aligned pairs
-          const double2 v = *reinterpret_cast<const double2*>(ct + j * LDT + i0 + r);
+        for (int r = 0; r < RPT; r += 2) {        // row pairs are even-aligned: 16-byte aligned loads
+          const double2 v = *reinterpret_cast<const double2*>(ct + j * LDT + rows_t[r]);
           a[r] = v.x;
           a[r + 1] = v.y;
         }
@@ -676,10 +776,23 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[r][q] = fma(a[r], bb[q], acc[r][q]);
     }
+    if constexpr (RPT == 4) {
+#pragma unroll 4
+      for (int j = jsplit; j < jend; ++j) {          // balanced lower: the high rows only
+        const float4 b = *reinterpret_cast<const float4*>(ins + j * AT_COLS + cg * 4);
+        const double2 v = *reinterpret_cast<const double2*>(ct + j * LDT + rows_t[2]);
+        const double bb[4] = {(double)b.x, (double)b.y, (double)b.z, (double)b.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2][q] = fma(v.x, bb[q], acc[2][q]);
+          acc[3][q] = fma(v.y, bb[q], acc[3][q]);
+        }
+      }
+    }
     const int64_t x0 = ch * AT_COLS + cg * 4;
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-      const int i = i0 + r;
+      const int i = rows_t[r];
       if (i >= rows) continue;
       const int oi = row_map ? row_map[i] : i;
       if (oi < 0) continue;

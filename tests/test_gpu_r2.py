@@ -435,3 +435,101 @@ def test_theorem1_assertion_vs_oracle(P, ctx):
         # angles from fp32 unit rows (acos of |⟨e, t⟩|): resolved to ~5e-4 near zero
         np.testing.assert_allclose(ap, ap_ref, atol=1e-3)
         np.testing.assert_allclose(aq, aq_ref, atol=1e-3)
+
+
+# ----------------------------------------------------------------------------- huge d (NEXT-3)
+C6M = C.Workload("C6m", G.GenSpec("planted_householder", n=1_100, d=524_288, seed=1005, spectrum="power", a=1.0,
+                                  relu=True, house_r=8, dtype="bf16"),
+                 k=8, l=0, priming="eigengame", batch=1024, alpha=1e-2, steps=4, init_seed=2005)
+
+
+def test_huge_d_eigengame_and_refine_vs_oracle(P, ctx):
+    """The paper's large-scale regime (P L373-381: d ~ 13M, EigenGame batch 1024, k = 8, pPCA without extra
+    components, 10 % projection) at d = 524288 with few rows: K-split window passes (8192 K chunks), 4096
+    d-groups in kernel B, the K-split refine pass (fewer row tiles than SMs) and the sampled refine — the same
+    kernel paths the 13.1M-dim tool run takes — against the oracle."""
+    import torch
+    w = C6M
+    s = w.spec
+    Xs = G.dataset(s)
+    X64 = G.stored_to_f64(Xs, s.dtype)
+    Xm = _device(P, ctx, Xs, s, False)
+    del Xs
+    V_ref, _ = O.prime_eigengame(X64, G.init_gaussians(w.init_seed, w.m, s.d), w.batch, w.alpha, w.momentum, w.steps)
+    V = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+    vel = torch.zeros_like(V)
+    P.ppca_prime_eigengame(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, w.steps, w.init_seed, V, vel, 0)
+    Vh = V.cpu().numpy().astype(np.float64)
+    rel = np.linalg.norm(Vh - V_ref) / np.linalg.norm(V_ref)
+    V0 = O.init_vectors(G.init_gaussians(w.init_seed, w.m, s.d))
+    moved = np.linalg.norm(V_ref - V0) / np.linalg.norm(V0)
+    print(f"\n[huge-d] d={s.d}: EigenGame drift {rel:.2e} (trajectory moved {moved:.2e})")
+    assert rel < 1e-3 and moved > 1e-2
+    E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, V_ref, w.k)
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    th, dim = P.ppca_refine(ctx, Xm, V, w.m, w.k, E)
+    err = U.ritz_rel_err(th, th_ref)
+    print(f"[huge-d] refine Ritz rel err {err:.2e}")
+    assert err < 1e-3
+    gi = U.gapped(th_all_ref, w.k)
+    if gi.size:
+        assert U.abs_cos(E.cpu().numpy()[gi], E_ref[gi]).min() >= 0.9999
+    # the paper's 10 % projection (P L378, R25): same seeded tiles on both sides
+    E2, th2r, used_ref = O.ppca_refine_sampled(X64, V_ref, w.k, 0.5, 77)
+    th2, _, used = P.ppca_refine_sampled(ctx, Xm, V, w.m, w.k, E, 0.5, 77)
+    assert used == used_ref
+    assert U.ritz_rel_err(th2, th2r) < 1e-3
+
+
+# ----------------------------------------------------------------------------- distributed CholQR (§6)
+def _power_run(P, h, s, w, iters, split):
+    import torch
+    X = torch.empty((s.n, s.d), dtype=torch.bfloat16 if s.dtype == "bf16" else torch.float32, device="cuda")
+    P.ppca_generate(h, P.gen_spec(s, split=s.dtype == "f32"), X)
+    Xm = P.matrix(X, split=s.dtype == "f32")
+    P.ppca_set_orth_split(h, split)
+    P.ppca_set_pass_impl(h, 2)
+    try:
+        W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+        c0 = P.ppca_collective_count(h)
+        th = P.ppca_prime_power(h, Xm, w.m, iters, w.init_seed, W, theta_hist=True)
+        return th, W.cpu().numpy(), P.ppca_collective_count(h) - c0
+    finally:
+        P.ppca_set_orth_split(h, 0)
+        P.ppca_set_pass_impl(h, 0)
+
+
+def test_distributed_orth_nccl_path_one_rank_bitwise(P):
+    """The d-sliced CholQR's NCCL path (reduce-scatter of Z + all-reduce of S in one group, slice Gram, m×m
+    all-reduce, slice apply, all-gather of W) over a one-rank communicator: bitwise the replicated CholQR, three
+    NCCL operations per iteration."""
+    import torch
+    w = C.SMALL["C5s"]
+    s = w.spec
+    stream = torch.cuda.current_stream()
+    plain = P.ppca_ctx_create(0, stream)
+    comm = P.ppca_ctx_create_one_rank_comm(0, stream)
+    try:
+        th0, W0, n0 = _power_run(P, plain, s, w, 4, 0)
+        th1, W1, n1 = _power_run(P, comm, s, w, 4, -1)
+    finally:
+        P.ppca_ctx_destroy(plain)
+        P.ppca_ctx_destroy(comm)
+    assert n0 == 0 and n1 == 3 * 4, f"collectives {n0} / {n1}"
+    assert np.array_equal(th0, th1) and np.array_equal(W0, W1)
+
+
+@pytest.mark.parametrize("blocks", [2, 4])
+def test_distributed_orth_emulated_slices_match(P, ctx, blocks):
+    """b emulated d-slices on one GPU (the blocked Z layout, slice Grams summed, slice applies, the unblocking):
+    the same CholQR up to the Gram's summation order, and the oracle's per-iterate Ritz values (C5s, bf16)."""
+    w = C.SMALL["C5s"]
+    s = w.spec
+    th0, W0, _ = _power_run(P, ctx, s, w, 4, 1)
+    th1, W1, _ = _power_run(P, ctx, s, w, 4, blocks)
+    assert U.ritz_rel_err(th1, th0) < 1e-6
+    assert np.max(np.abs(W1 - W0)) < 1e-5
+    X64 = G.dataset_f64(s)
+    _, S_hist = O.prime_power(X64, G.init_gaussians(w.init_seed, w.m, s.d), 4)
+    for t in range(4):
+        assert U.ritz_rel_err(th1[t], O.ritz_values(S_hist[t])) < 1e-3
