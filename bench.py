@@ -319,8 +319,10 @@ def run_ours(args, w, rank, world, local_rank):
     kb_elt = 2 if (split or s.dtype == "bf16") else 4
     kernels = []
     if ka_n and not kb_n:                              # the single-read fused power pass (one kernel)
-        kernels.append(("xwz_fused_kernel (single-read power pass: Y = X W'^T, S = Y^T Y, Z^T = X^T Y)",
-                        ka_ms_tot, ka_n, per_rank_bytes))
+        fk = ("xwz_pair_kernel (single-read power pass on d-sliced CTA pairs: Y = X W'^T, S = Y^T Y, Z^T = X^T Y)"
+              if P.ppca_last_power_kernel(ctx) == 4 else
+              "xwz_fused_kernel (single-read power pass, row groups: Y = X W'^T, S = Y^T Y, Z^T = X^T Y)")
+        kernels.append((fk, ka_ms_tot, ka_n, per_rank_bytes))
     elif ka_n:
         kernels.append(("xw_tma_kernel (kernel A2: Y = X W'^T, S = Y^T Y)" if s.dtype != "f32" or split
                         else "xw_tc_kernel (kernel A: Y = X W'^T, S = Y^T Y)", ka_ms_tot, ka_n, per_rank_bytes))

@@ -264,7 +264,8 @@ ppca_status ppca_get_pass_time(ppca_ctx* ctx, double* ms_total, int64_t* passes)
 ppca_status ppca_get_kernel_time(ppca_ctx* ctx, int which, double* ms_total, int64_t* launches);
 
 /* Timing hook: select the fused-pass implementation (0 = auto, 1 = SIMT fp32, 2 = tcgen05, 3 = tcgen05
- * with the power pass as two kernels instead of the single-read fused kernel; 3 reports as 2).
+ * with the power pass as two kernels instead of a single-read fused kernel, 4 = tcgen05 with the power pass
+ * on the row-group fused kernel (round 1) instead of the d-sliced pair kernel; 3 and 4 report as 2).
  * Returns UNSUPPORTED if the requested path cannot run this matrix. */
 ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);
 /* Re-orthonormalisation of the power iteration: 0 = auto — with world > 1 and d·m² ≥ 2^28 (C5)
@@ -275,6 +276,10 @@ ppca_status ppca_set_pass_impl(ppca_ctx* ctx, int impl);
 ppca_status ppca_set_orth_split(ppca_ctx* ctx, int split);
 /* Implementation used by the most recent pass (1 = SIMT, 2 = tcgen05; 0 = none yet). */
 int ppca_last_pass_impl(const ppca_ctx* ctx);
+/* Kernels of the most recent tensor-core power pass (bench.py's roofline label): 2 = kernel A2 + kernel B
+ * (X read twice), 3 = the row-group single-read kernel (xwz_fused_kernel), 4 = the d-sliced pair single-read
+ * kernel (xwz_pair_kernel); 0 = none yet. */
+int ppca_last_power_kernel(const ppca_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
+           "ppca_last_pass_impl", "ppca_last_power_kernel", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
            "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals", "ppca_refine_ex",
            "ppca_check_theorem1", "ppca_set_orth_split"]
 
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "ppca_set_pass_impl": (I, [P, I]),
         "ppca_set_timing": (I, [P, I]),
         "ppca_last_pass_impl": (I, [P]),
+        "ppca_last_power_kernel": (I, [P]),
         "ppca_get_pass_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "ppca_split_f32": (I, [P, P, I64, I64, I64]),
         "ppca_refine_sampled": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, D, ctypes.c_uint64, P, P,
@@ -263,6 +264,10 @@ def ppca_set_pass_impl(ctx, impl: int) -> None:
 
 def ppca_last_pass_impl(ctx) -> int:
     return int(load().ppca_last_pass_impl(ctx))
+
+
+def ppca_last_power_kernel(ctx) -> int:
+    return int(load().ppca_last_power_kernel(ctx))
 
 
 def ppca_set_timing(ctx, enable: bool) -> None:

@@ -25,29 +25,33 @@ def _newer(src_list, target):
     return any(os.path.getmtime(s) > t for s in src_list)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, experiments: bool = False) -> str:
+    """Compile the library.  experiments=True builds libppca_exp.so (-DPPCA_EXPERIMENTS: tuning switches read
+    from the environment) for the tools/ ablations; the product library is always libppca.so without it."""
+    build_dir, lib, extra = BUILD, LIB, []
+    if experiments:
+        build_dir, lib, extra = BUILD + "_exp", LIB.replace("libppca.so", "libppca_exp.so"), ["-DPPCA_EXPERIMENTS"]
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ppca.h"))
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer([s] + headers, o):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _newer(objs, LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
+    if force or _newer(objs, lib):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, experiments="--experiments" in sys.argv))

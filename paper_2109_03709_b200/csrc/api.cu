@@ -437,8 +437,10 @@ ppca_status ppca_debug_wait_counters(unsigned long long* out16) { return ppca::d
 
 int ppca_last_pass_impl(const ppca_ctx* h) { return h ? h->c.last_impl : -1; }
 
+int ppca_last_power_kernel(const ppca_ctx* h) { return h ? h->c.last_power_kernel : -1; }
+
 ppca_status ppca_set_pass_impl(ppca_ctx* h, int impl) {
-  if (!h || impl < 0 || impl > 3) return PPCA_ERR_INVALID_ARG;
+  if (!h || impl < 0 || impl > 4) return PPCA_ERR_INVALID_ARG;
   h->c.pass_impl = impl;
   return PPCA_OK;
 }

@@ -51,6 +51,7 @@ struct Ctx {
   int64_t flags_n = 0;
   int epoch = 0;
   int last_impl = 0;                  // implementation of the most recent pass
+  int last_power_kernel = 0;          // kernels of the most recent tensor-core power pass (ppca_last_power_kernel)
   int sm_count = 148;
   int64_t launches = 0;
   int64_t collectives = 0;            // NCCL operations enqueued (bench evidence of the exchange)

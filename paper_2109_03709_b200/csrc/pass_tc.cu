@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
 
 // ============================================================================ fused power pass (tc_fused.cuh)
 #include "tc_fused.cuh"
+#include "tc_pair.cuh"
 
 // ============================================================================ kernel B (tc_xty.cuh)
 #include "tc_xty.cuh"
@@ -608,7 +609,8 @@ static cudaError_t launch_fused_cfg(Ctx* c, int cfg, int grid, const CUtensorMap
 // The single-read power pass: TMA-staged X (bf16 / split), m ≤ 64 (padded to 64), d ≤ KSEG·BK (one
 // accumulation segment), a whole row tile per CTA at least.
 static bool fused_eligible(const Ctx* c, const ppca_matrix* X, int mp, bool precise) {
-  return c->pass_impl != 3 && !precise && X->dtype != PPCA_F32 && mp == 64 && X->d <= ka2::KSEG * ka2::BK &&
+  return (c->pass_impl == 0 || c->pass_impl == 2 || c->pass_impl == 4) && !precise && X->dtype != PPCA_F32 && mp == 64 &&
+         X->d <= ka2::KSEG * ka2::BK &&
          X->n_local >= 128;
 }
 
@@ -708,6 +710,125 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   return PPCA_OK;
 }
 
+// ============================================================================ d-sliced pair pass (tc_pair.cuh)
+template <int XM, int NSTA, int NWS, int NSTB, int KR>
+static constexpr size_t pair_smem() {
+  return 1024 + (size_t)NSTA * (XM == 2 ? 2 * kp2::XPL : kp2::XPL) + (size_t)NWS * kp2::WST +
+         (size_t)NSTB * kp2::NCH * KR * 128 + 2 * kp2::YSL + 256;
+}
+
+// Clusters of 2 (a pair's waits never leave the cluster, which is co-scheduled by construction)
+template <int XM, int NSTA, int NWS, int NSTB, int KR>
+static cudaError_t launch_pair(Ctx* c, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                               const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const KP2Params& pp) {
+  constexpr size_t smem = pair_smem<XM, NSTA, NWS, NSTB, KR>();
+  static_assert(smem <= 227 * 1024, "pair kernel shared memory budget");
+  auto kern = xwz_pair_kernel<XM, NSTA, NWS, NSTB, KR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kp2::NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmXlo, tmXb, pp);
+}
+
+template <int XM>
+static cudaError_t launch_pair_cfg(Ctx* c, int cfg, int grid, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                                   const CUtensorMap& tmXlo, const CUtensorMap& tmXb, const KP2Params& pp) {
+  // (X stages, W' stages, B stages, rows per B stage); PPCA_PAIR_CFG (experiment builds) selects the others
+  switch (cfg) {
+    case 1: return launch_pair<XM, 2, 2, 2, 32>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+    case 2: return launch_pair<XM, 2, 2, 3, 16>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+    case 3: return launch_pair<XM, 2, 3, 3, 16>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+    case 4: return launch_pair<XM, 3, 1, 3, 16>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+    case 5: return launch_pair<XM, 2, 2, 4, 16>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+    default: return launch_pair<XM, 3, 2, 2, 16>(c, grid, tmW, tmX, tmXlo, tmXb, pp);
+  }
+}
+
+// The d-sliced pair pass: TMA-staged X (bf16 / split), m ≤ 64 (padded to 64), SL < d ≤ 2·SL, whole tiles.
+static bool pair_eligible(const Ctx* c, const ppca_matrix* X, int mp, bool precise) {
+  return (c->pass_impl == 0 || c->pass_impl == 2) && !precise && X->dtype != PPCA_F32 && mp == 64 &&
+         X->d > kp2::SL && X->d <= 2 * kp2::SL && X->n_local >= 128 && persistent_ctas(c) >= 2;
+}
+
+static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb, int m, float* Z, double* S) {
+  const int mp = 64;
+  const int64_t n = X->n_local, d = X->d;
+  const int64_t ntiles = ceil_div(n, kp2::BM);
+  int nrg = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c) / 2, ntiles));
+  const int64_t tpr = ceil_div(ntiles, (int64_t)nrg);
+  nrg = (int)ceil_div(ntiles, tpr);
+  const int grid = 2 * nrg;
+  double* Spart = (double*)scratch(c, S_TC0, (size_t)grid * 2 * mp * mp * sizeof(double));
+  const int64_t dpad = 2 * kp2::SL;
+  float* Zp = (float*)scratch(c, S_PART, (size_t)nrg * dpad * mp * sizeof(float));
+  if (!Spart || !Zp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  CUtensorMap tmW, tmX, tmXlo, tmXb, tmXblo;
+  if (!make_map_bf16(&tmW, Wb, d, 2 * mp, d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
+  tmXlo = tmW;
+  static int cfg = -1;
+  if (cfg < 0) cfg = tune_env("PPCA_PAIR_CFG", 0);
+  const uint32_t kr = (cfg == 1) ? 32 : 16;
+  if (!make_x_maps(X, kp2::BM, &tmX, &tmXlo) || !make_x_maps(X, kr, &tmXb, &tmXblo))
+    return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
+  KP2Params pp;
+  pp.n = n; pp.d = d; pp.ntiles = ntiles; pp.nrg = nrg; pp.tiles_per_rg = tpr;
+  pp.Spart = Spart; pp.Zp = Zp; pp.trace = nullptr;
+#ifdef PPCA_EXPERIMENTS
+  static int trace_at = -1, launches = 0;         // PPCA_TRACE=k: stamp the k-th launch, dump it to gpurun_out/
+  if (trace_at < 0) trace_at = tune_env("PPCA_TRACE", 0);
+  static long long* tbuf = nullptr;
+  const size_t tbytes = ((size_t)2 * KP2_TRACE_TILES * KP2_TRACE_EV + 2 * 1024) * sizeof(long long);
+  const bool tracing = trace_at > 0 && ++launches == trace_at;
+  if (tracing) {
+    if (!tbuf) cudaMalloc(&tbuf, tbytes);
+    cudaMemsetAsync(tbuf, 0, tbytes, c->stream);
+    pp.trace = tbuf;
+  }
+#endif
+  if (c->s_defer) cudaStreamWaitEvent(c->stream, c->s_ev_red, 0);   // the previous S partials were reduced
+  kernel_timer_mark(c, 0);
+  const cudaError_t le = X->dtype == PPCA_F32_SPLIT ? launch_pair_cfg<2>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, pp)
+                                                    : launch_pair_cfg<1>(c, cfg, grid, tmW, tmX, tmXlo, tmXb, pp);
+  if (le != cudaSuccess) return check_cuda(c, le, "xwz_pair_kernel");
+  PPCA_LAUNCH_CHECK(c, "xwz_pair_kernel");
+#ifdef PPCA_EXPERIMENTS
+  if (tracing) {
+    std::vector<long long> hbuf(tbytes / sizeof(long long));
+    cudaMemcpyAsync(hbuf.data(), tbuf, tbytes, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    if (FILE* f = fopen("gpurun_out/pair_trace.bin", "wb")) {
+      fwrite(hbuf.data(), 1, tbytes, f);
+      fclose(f);
+    }
+  }
+#endif
+  kernel_timer_mark(c, 0);
+  if (c->s_defer) {                               // S is reduced later, on the stream that consumes it
+    cudaEventRecord(c->s_ev_pass, c->stream);
+    c->s_pending = true;
+    c->s_part = Spart;
+    c->s_parts = grid;
+    c->s_mp = mp;
+    c->s_m = m;
+  } else {
+    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  }
+  launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
+  PPCA_LAUNCH_CHECK(c, "reduce_zp");
+  return PPCA_OK;
+}
+
 ppca_status pass_reduce_deferred_s(Ctx* c, double* S, cudaStream_t st) {
   if (!c->s_pending) return PPCA_OK;
   cudaStreamWaitEvent(st, c->s_ev_pass, 0);
@@ -730,17 +851,26 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   // rows of a split X the pass adds X_lo·Y_hi (kernel B's XLO instantiation) — the cost is nil at that size
   constexpr int64_t kPreciseRows = 32768;
   precise = precise || (X->dtype == PPCA_F32_SPLIT && X->n_global < kPreciseRows);
-  const bool fused = fused_eligible(c, X, mp, precise);
-  // bf16 X outside the fused kernel and outside the minibatch steps: product 2 with Y_hi alone (R27)
-  const bool lean = X->dtype == PPCA_BF16 && !fused && !precise;
+  const bool pair = pair_eligible(c, X, mp, precise);
+  const bool fused = !pair && fused_eligible(c, X, mp, precise);
+  // bf16 X outside the fused kernels and outside the minibatch steps: product 2 with Y_hi alone (R27)
+  const bool lean = X->dtype == PPCA_BF16 && !fused && !pair && !precise;
   PPCA_TRY(prep_w(c, W, m, mp, d, &Wb, &Wr));
   const_cast<PassPlan*>(plan)->Wop = Wr;
   if (c->prep_ev) cudaEventRecord(c->prep_ev, c->stream);     // W' ready: the side stream may read Wr
+  if (pair) {
+    c->last_power_kernel = 4;
+    return pass_pair_power(c, X, Wb, m, Z, S);
+  }
   if (fused) {
     bool launched = false;
     PPCA_TRY(pass_fused_power(c, X, Wb, m, Z, S, &launched));
-    if (launched) return PPCA_OK;
+    if (launched) {
+      c->last_power_kernel = 3;
+      return PPCA_OK;
+    }
   }
+  c->last_power_kernel = 2;
   // Yᵀ as a bf16 pair [Y_hi; Y_lo], [2·mp][ldyt]; kernel A writes every row and column < ldyt
   const int64_t ldyt = ceil_div(n, 64) * 64;
   __nv_bfloat16* YT = (__nv_bfloat16*)scratch(c, S_Y, (size_t)2 * mp * ldyt * 2);

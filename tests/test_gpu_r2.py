@@ -110,20 +110,51 @@ C4M = dataclasses.replace(C.C4, name="C4m", spec=dataclasses.replace(C.C4.spec, 
 C5M = dataclasses.replace(C.C5, name="C5m", spec=dataclasses.replace(C.C5.spec, n=6_007), iters=3)
 
 
-def test_c3m_fused_pass_four_dgroups_vs_oracle(P, ctx):
-    """d = 1024: the fused kernel runs 4 d-groups per row group (cross-CTA per-tile flags, Y rows through
-    global memory, X_hi re-read from L2) — the launch configuration of full-size C3 — against the oracle."""
+@pytest.mark.parametrize("impl", [0, 4], ids=["pair", "rowgroup"])
+def test_c3m_fused_pass_vs_oracle(P, ctx, impl):
+    """d = 1024, the launch configuration of full-size C3, against the oracle: impl 0 (auto) runs the d-sliced
+    pair kernel (two 512-column slices per row group, Y exchanged through distributed shared memory); impl 4
+    the row-group kernel (4 d-groups per row group, per-tile flags, Y rows through global memory, X_hi re-read
+    from L2 by the siblings)."""
     w = C3M
     Xs = G.dataset(w.spec)
     X64 = G.stored_to_f64(Xs, w.spec.dtype)
     lam, T = _top_truth(X64, w.k)
     Xm = _device(P, ctx, Xs, w.spec, True)
-    P.ppca_set_pass_impl(ctx, 0)
+    P.ppca_set_pass_impl(ctx, impl)
 
     def only_fused(ka, kb):
         assert ka == w.iters and kb == 0, f"expected the single-read fused kernel only (A {ka}, B {kb})"
 
-    _power_parity(P, ctx, Xm, X64, w, w.iters, T, only_fused)
+    try:
+        _power_parity(P, ctx, Xm, X64, w, w.iters, T, only_fused)
+        assert P.ppca_last_power_kernel(ctx) == (4 if impl == 0 else 3)
+    finally:
+        P.ppca_set_pass_impl(ctx, 0)
+
+
+PAIR_RAGGED = [
+    # split fp32, d = 800: slice 1 holds 288 columns (5 chunks, 3 d-chunks of 128, the last one partial)
+    dataclasses.replace(C.C3, name="C3r", spec=dataclasses.replace(C.C3.spec, n=40_007, d=800), iters=4),
+    # bf16, d = 576: slice 1 holds 64 columns (1 chunk, 1 d-chunk); a ragged last row tile
+    dataclasses.replace(C.C5, name="C5r", k=32, l=32, spec=dataclasses.replace(C.C5.spec, n=9_001, d=576), iters=3),
+]
+
+
+@pytest.mark.parametrize("w", PAIR_RAGGED, ids=[x.name for x in PAIR_RAGGED])
+def test_pair_pass_ragged_slices_vs_oracle(P, ctx, w):
+    """The d-sliced pair kernel where the second slice is partial (d not a multiple of 512) and the row count
+    is not a multiple of the 128-row tile, against the oracle."""
+    Xs = G.dataset(w.spec)
+    X64 = G.stored_to_f64(Xs, w.spec.dtype)
+    lam, T = _top_truth(X64, w.k)
+    Xm = _device(P, ctx, Xs, w.spec, w.spec.dtype == "f32")
+    P.ppca_set_pass_impl(ctx, 2)                 # the tensor-core path even where auto picks the CUDA cores
+    try:
+        _power_parity(P, ctx, Xm, X64, w, w.iters, T,
+                      lambda ka, kb: (ka == w.iters and kb == 0) or pytest.fail(f"A {ka} B {kb}"))
+    finally:
+        P.ppca_set_pass_impl(ctx, 0)
 
 
 def test_c3m_two_kernel_pass_matches_oracle(P, ctx):
