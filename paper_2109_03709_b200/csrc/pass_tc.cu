@@ -168,11 +168,8 @@ __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __rest
 // ============================================================================ kernel B (tc_xty.cuh)
 #include "tc_xty.cuh"
 
-// Z[j][x] = Σ_g Zp[g][x][j], g in order (fixed, deterministic).  Block = ZP_XB columns × all mp features:
-// the block's slice of each partial is ZP_XB·mp contiguous floats, read coalesced, with the partials of
-// 8 row groups in flight per thread; the sums leave through shared memory as ZP_XB-float runs of Z's rows.
-// (for many row groups — the fused power pass, nrg ≈ 36 — the per-column kernel below is faster: its
-// 8 warps split the partials; this one serves the short windows of the minibatch steps, nrg ≤ 16)
+// Z[j][x] = Σ_g Zp[g][x][j], g in order (fixed, deterministic): two kernels, for many row groups (the fused
+// power passes, nrg ≈ 36-74: 8 warps split the partials of a column) and for few (the minibatch windows).
 // Z[j][x] = Σ_g Zp[g][x][j]: block (x, 32 consecutive j), warp w sums g ≡ w (mod 8) (8 loads in flight),
 // the 8 warp sums are added in warp order.
 // Z's layout: plain [m][d] (ds = d) or d-blocked [d/ds][m][ds] (the slices of the distributed CholQR, §6):
@@ -199,43 +196,38 @@ __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __rest
   }
 }
 
-// ZP_XB columns × all mp features per block (≤ 16 elements per thread), the partials of 4 row groups in flight;
-// the sums leave through shared memory as ZP_XB-float (128-byte) runs of Z's rows
-constexpr int ZP_XB = 32;
+// Z[j][x] = Σ_g Zp[g][x][j] for a few row groups (the short windows of the minibatch steps, nrg ≤ 16): thread =
+// 4 consecutive features of one column (one float4 per partial, all nrg loads in flight), sums in g order in
+// fp64; a block covers 256·4/mp columns and leaves through shared memory as runs of Z's rows.
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z, int64_t ds) {
-  __shared__ float tr[128][ZP_XB + 1];
-  const int64_t x0 = (int64_t)blockIdx.x * ZP_XB;
-  const int cnt = ZP_XB * mp;                        // ≤ 4096: ≤ 16 elements per thread
-  const int64_t xrem = (d - x0) * mp;                // elements of the block inside [0, d)
-  const float* base = Zp + x0 * mp;
-  const int64_t gstride = dpad * mp;
-  double acc[16];
+  __shared__ float tr[128][65];
+  const int tpc = mp >> 2;                           // threads per column (mp ≤ 128, multiple of 16)
+  const int cpb = 256 / tpc;                         // columns per block (≤ 64)
+  const int64_t x0 = (int64_t)blockIdx.x * cpb;
+  const int xl = threadIdx.x / tpc, j4 = (threadIdx.x % tpc) * 4;
+  const int64_t x = x0 + xl;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (x < d) {
+    const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
+    const int64_t gs = dpad * mp / 4;
+    for (int64_t g0 = 0; g0 < nrg; g0 += 16) {
+      float4 v[16];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
-  for (int64_t g0 = 0; g0 < nrg; g0 += 4) {
-    float v[4][16];
+      for (int gg = 0; gg < 16; ++gg)
+        if (g0 + gg < nrg) v[gg] = __ldg(src + (g0 + gg) * gs);
 #pragma unroll
-    for (int gg = 0; gg < 4; ++gg)
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int e = threadIdx.x + 256 * u;
-        v[gg][u] = (g0 + gg < nrg && e < cnt && e < xrem) ? base[(g0 + gg) * gstride + e] : 0.f;
-      }
-#pragma unroll
-    for (int gg = 0; gg < 4; ++gg)
-#pragma unroll
-      for (int u = 0; u < 16; ++u) acc[u] += (double)v[gg][u];
+      for (int gg = 0; gg < 16; ++gg)
+        if (g0 + gg < nrg) {
+          a0 += (double)v[gg].x; a1 += (double)v[gg].y; a2 += (double)v[gg].z; a3 += (double)v[gg].w;
+        }
+    }
   }
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int e = threadIdx.x + 256 * u;
-    if (e < cnt) tr[e % mp][e / mp] = (float)acc[u];
-  }
+  tr[j4][xl] = (float)a0; tr[j4 + 1][xl] = (float)a1; tr[j4 + 2][xl] = (float)a2; tr[j4 + 3][xl] = (float)a3;
   __syncthreads();
-  for (int e = threadIdx.x; e < m * ZP_XB; e += 256) {
-    const int j = e / ZP_XB, xl = e % ZP_XB;
-    if (x0 + xl < d) Z[z_index(j, x0 + xl, m, ds)] = tr[j][xl];
+  for (int e = threadIdx.x; e < m * cpb; e += 256) {
+    const int j = e / cpb, c = e % cpb;
+    if (x0 + c < d) Z[z_index(j, x0 + c, m, ds)] = tr[j][c];
   }
 }
 
@@ -245,7 +237,7 @@ static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad,
     reduce_zp_cols_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z,
                                                                                             ds);
   else
-    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)ZP_XB), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z, ds);
+    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)(256 / (mp / 4))), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z, ds);
 }
 
 // ============================================================================ host side

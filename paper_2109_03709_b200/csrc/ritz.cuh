@@ -182,10 +182,12 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
 // eigenvalues of the tridiagonal by Sturm-count multisection (nt/m threads per eigenvalue, 5 sub-intervals
 // per round).  O(m³/nt + m²) instead of Jacobi's O(sweeps·m) barrier rounds.
 //
-// With R != nullptr (m ≤ 64: the refine) the eigenvectors follow too: inverse iteration on the tridiagonal
-// (Gaussian elimination with partial pivoting, 3 steps, clusters of eigenvalues closer than 1e-9·‖T‖ handled
-// by one thread with Gram–Schmidt against the cluster's earlier vectors at every step), back-transformation
-// by the stored Householder reflectors (one thread per vector), then R = Uᵀ L⁻¹ in descending order.
+// With R != nullptr (m ≤ 64: the refine) the eigenvectors follow too: one thread per eigenvalue solves the
+// twisted factorization of T − θI (top-down LDLᵀ and bottom-up UDUᵀ pivots in shared memory, twist index at
+// the smallest |γ_r|, one substitution each way — no iteration); clusters of eigenvalues closer than
+// 1e-9·‖T‖ keep inverse iteration (Gaussian elimination with partial pivoting, 3 steps, Gram–Schmidt against
+// the cluster's earlier vectors at every step, one thread per cluster); back-transformation by the stored
+// Householder reflectors, then R = Uᵀ L⁻¹ in descending order.
 __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
                                                           int m, double* __restrict__ gLinv, double* __restrict__ gT1,
                                                           double* __restrict__ theta, int* d_err,
@@ -368,10 +370,53 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   // one serial Gram–Schmidt chain (8.5 ms per refine, measured)
   const double ctol = 1e-9 * fmax(fabs(lo), fabs(hi));
   const double tiny = 1e-14 * span;
+  double* Dp = A + 3 * m * m;                         // Dp[i·m + j], Dm[i·m + j]: pivots of eigenvalue j's twist
+  double* Dm = A + 4 * m * m;
   for (int j0 = tid; j0 < m; j0 += nt) {
     if (j0 > 0 && evals[j0] - evals[j0 - 1] <= ctol) continue;   // not a cluster leader
     int j1 = j0 + 1;
     while (j1 < m && evals[j1] - evals[j1 - 1] <= ctol) ++j1;
+    if (j1 == j0 + 1) {
+      // isolated eigenvalue: twisted factorization  T − σI = L₊D₊L₊ᵀ = U₋D₋U₋ᵀ,  γ_r = D₊_r + D₋_r − (a_r − σ);
+      // z_r = 1, z_i = −(b_i / D₊_i)·z_{i+1} above r, z_i = −(b_{i−1} / D₋_i)·z_{i−1} below r
+      const int j = j0;
+      const double sg = evals[j];
+      auto guard = [&](double v) { return fabs(v) < tiny ? (v < 0.0 ? -tiny : tiny) : v; };
+      double dp = guard(ta[0] - sg);
+      Dp[j] = dp;
+      for (int i = 1; i < m; ++i) {
+        dp = guard((ta[i] - sg) - tb[i - 1] * (tb[i - 1] / dp));
+        Dp[i * m + j] = dp;
+      }
+      double dm = guard(ta[m - 1] - sg);
+      Dm[(m - 1) * m + j] = dm;
+      for (int i = m - 2; i >= 0; --i) {
+        dm = guard((ta[i] - sg) - tb[i] * (tb[i] / dm));
+        Dm[i * m + j] = dm;
+      }
+      int r = 0;
+      double gbest = 1e300;
+      for (int i = 0; i < m; ++i) {
+        const double g = fabs(Dp[i * m + j] + Dm[i * m + j] - (ta[i] - sg));
+        if (g < gbest) { gbest = g; r = i; }
+      }
+      double z = 1.0, nn = 1.0;
+      XT[r * m + j] = 1.0;
+      for (int i = r - 1; i >= 0; --i) {
+        z = -(tb[i] / Dp[i * m + j]) * z;
+        XT[i * m + j] = z;
+        nn = fma(z, z, nn);
+      }
+      z = 1.0;
+      for (int i = r + 1; i < m; ++i) {
+        z = -(tb[i - 1] / Dm[i * m + j]) * z;
+        XT[i * m + j] = z;
+        nn = fma(z, z, nn);
+      }
+      const double rn = rsqrt(nn);
+      for (int i = 0; i < m; ++i) XT[i * m + j] *= rn;
+      continue;
+    }
     for (int j = j0; j < j1; ++j) {
       double dl[PPCA_MAX_M / 2], d[PPCA_MAX_M / 2], du[PPCA_MAX_M / 2], du2[PPCA_MAX_M / 2], x[PPCA_MAX_M / 2];
       bool sw[PPCA_MAX_M / 2];
@@ -472,6 +517,8 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
 }
 
 inline size_t values_smem_bytes(int m) { return (size_t)(m <= 64 ? 3 : 1) * m * m * sizeof(double); }
+// with eigenvectors (m ≤ 64): + the twisted factorizations' pivots (2 · m × m)
+inline size_t vectors_smem_bytes(int m) { return (size_t)5 * m * m * sizeof(double); }
 
 inline size_t smem_bytes(int m) {
   const int mm = (m + 1) & ~1;

@@ -937,10 +937,10 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
   if (!R_dev || (m <= 64 && !jacobi)) {           // tridiagonalisation + multisection (+ inverse iteration)
     static uint64_t vattr = 0;
     if (first_on_device(&vattr, c->device)) {
-      cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);   // + 32 KB static
     }
-    ritz::ritz_values_kernel<<<1, 512, ritz::values_smem_bytes(m), stream>>>(S, Bm, m, scr, scr + (size_t)m * m,
-                                                                              theta_dev, c->d_err, R_dev);
+    const size_t vsm = (R_dev && m <= 64) ? ritz::vectors_smem_bytes(m) : ritz::values_smem_bytes(m);
+    ritz::ritz_values_kernel<<<1, 512, vsm, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, c->d_err, R_dev);
     PPCA_LAUNCH_CHECK(c, "ritz_values_kernel");
     return PPCA_OK;
   }

@@ -151,6 +151,50 @@ def test_c3_full_size(P, ctx):
     _properties(P, ctx, Xm, w, W2, h2, E2, th2, tol)
 
 
+def test_c3_full_size_power_and_refine_vs_oracle(P, ctx):
+    """C3 (BASELINE configs[2]) at its full size, 10⁶ x 1024, against the fp64 oracle directly, in the bench's
+    launch configuration: the split layout, the d-sliced pair kernel (73–74 clusters over 1e6 rows), 4 block
+    power iterations from the seeded start (the time-to-LCES count) and the refine — per-iterate Ritz values
+    1e-4, the primed subspace, refine Ritz values / |cos| where gapped, identical LCES at all thresholds.
+    The oracle streams the stored X (the device generator's output, itself checked against the host
+    generator on sampled rows in test_c3_full_size) in fp64: ~8 GB of host memory, ~1 TFLOP of numpy."""
+    import torch
+    from oracle import ppca_oracle as O
+    w = C.C3
+    s = w.spec
+    iters = 4
+    X, mu = _gen(P, ctx, w, split=False)
+    X64 = X.cpu().numpy().astype(np.float64)
+    P.ppca_split_f32(ctx, X, s.d)
+    Xm = P.matrix(X, split=True)
+    W0 = G.init_gaussians(w.init_seed, w.m, s.d)
+    W_ref, S_hist = O.prime_power(X64, W0, iters)
+    E_ref, th_ref, th_all_ref, _ = O.ppca_refine(X64, W_ref, w.k)
+    G64 = X64.T @ X64
+    lam, V = np.linalg.eigh(G64)
+    T = O.sign_convention(V[:, ::-1][:, : w.k].T.copy())
+    del G64, X64
+    W = torch.zeros((w.m, s.d), dtype=torch.float32, device="cuda")
+    P.ppca_set_pass_impl(ctx, 0)
+    hist = P.ppca_prime_power(ctx, Xm, w.m, iters, w.init_seed, W, theta_hist=True)
+    assert P.ppca_last_power_kernel(ctx) == 4, "expected the d-sliced pair kernel (the bench's configuration)"
+    worst = 0.0
+    for t in range(iters):
+        e = U.ritz_rel_err(hist[t], O.ritz_values(S_hist[t]))
+        worst = max(worst, e)
+        assert e < 1e-4, f"C3 full iteration {t}: {e:.3e}"
+    Wh = W.cpu().numpy().astype(np.float64)
+    assert np.linalg.svd(Wh @ W_ref.T, compute_uv=False).min() > 1 - 1e-4
+    E = torch.zeros((w.k, s.d), dtype=torch.float32, device="cuda")
+    th, dim = P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
+    assert dim == w.m
+    err = U.assert_ppca_parity(E.cpu().numpy(), th, E_ref, th_ref, T, 1e-4, "C3 full", th_all_ref)
+    lc, _ = U.lces_all(E.cpu().numpy(), T)
+    lc_ref, _ = U.lces_all(E_ref, T)
+    assert lc == lc_ref, f"LCES {lc} vs oracle {lc_ref}"
+    print(f"\n[parity] C3 full: per-iterate Ritz err {worst:.2e}, refine {err:.3e}, LCES {lc}")
+
+
 def test_c5_full_size(P, ctx):
     """C5 (n = 2·10⁵, d = 65536, bf16, m = 128): generator rows, properties, tcgen05 vs CUDA-core pass."""
     w = C.C5

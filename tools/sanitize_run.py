@@ -1,5 +1,6 @@
 """Small runs of every hot-path kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
-the fused single-read power pass (cross-CTA flag protocol), the two-kernel pass, the K-split refine, the
+the d-sliced pair power pass (DSMEM bulk-copy exchange), the row-group fused pass (cross-CTA flag protocol),
+the two-kernel pass, the K-split refine, the
 persistent cooperative Oja kernel, the EigenGame window pass + cooperative update, the m×m chain.
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py
@@ -18,16 +19,18 @@ from inputs import configs as C  # noqa: E402
 def main():
     P.load()
     ctx = P.ppca_ctx_create(0, torch.cuda.current_stream())
-    # C3-like, d = 1024 (4 d-groups in the fused kernel), split layout
-    w = dataclasses.replace(C.C3, spec=dataclasses.replace(C.C3.spec, n=20_011))
+    # C3-like, d = 1024 (two 512-column slices in the pair kernel, 4 d-groups in the row-group kernel), split
+    # layout; ≥ 32768 rows, so the power pass is not the precise (small-shard) variant
+    w = dataclasses.replace(C.C3, spec=dataclasses.replace(C.C3.spec, n=40_011))
     s = w.spec
     X = torch.empty((s.n, s.d), dtype=torch.float32, device="cuda")
     P.ppca_generate(ctx, P.gen_spec(s, split=True), X)
     Xm = P.matrix(X, split=True)
     W = torch.empty((w.m, s.d), dtype=torch.float32, device="cuda")
-    for impl in (0, 3):                                     # fused pass, then the two-kernel pass
+    for impl, kern in ((0, 4), (4, 3), (3, 2)):             # pair kernel, row-group kernel, two kernels
         P.ppca_set_pass_impl(ctx, impl)
         P.ppca_prime_power(ctx, Xm, w.m, 2, w.init_seed, W, theta_hist=True)
+        assert P.ppca_last_power_kernel(ctx) == kern, (impl, P.ppca_last_power_kernel(ctx))
     P.ppca_set_pass_impl(ctx, 0)
     E = torch.empty((w.k, s.d), dtype=torch.float32, device="cuda")
     P.ppca_refine(ctx, Xm, W, w.m, w.k, E)
