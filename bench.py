@@ -373,9 +373,7 @@ def run_ours(args, w, rank, world, local_rank):
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(ke):
-            X.copy_(Xh, non_blocking=True)                             # the user's fp32 rows
-            if split:
-                P.ppca_split_f32(ctx, X, s.d)                             # → split layout (in place)
+            P.ppca_upload_rows(ctx, Xh, Xm)                               # the user's rows, host → HBM (+ split)
             P.ppca_prime_power(ctx, Xm, w.m, 1, 0, W, theta_hist=True)   # θ read back to the host
         e1.record(stream)
         torch.cuda.synchronize()

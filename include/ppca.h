@@ -139,6 +139,17 @@ ppca_status ppca_generate(ppca_ctx* ctx, const ppca_gen_spec* spec, void* X, int
  * PPCA_F32_SPLIT layout (same buffer, same ld).  Bit-exact: hi = RN_bf16(x), lo = RN_bf16(x − hi). */
 ppca_status ppca_split_f32(ppca_ctx* ctx, void* X, int64_t n_local, int64_t d, int64_t ld);
 
+/* Host → device upload of a block of X's rows (the end-to-end path: the user's data lives in host memory;
+ * P L14 "data X" in, no other preprocessing).  host: `rows` rows of X's logical element type with row stride
+ * ld_host elements — fp32 for PPCA_F32 and PPCA_F32_SPLIT, bf16 for PPCA_BF16 — pinned (asynchronous on the
+ * context stream) or pageable (staged by the driver).  They land in the device shard described by X at local
+ * row r0 (0 ≤ r0, r0 + rows ≤ X->n_local); for PPCA_F32_SPLIT the fp32 rows are then split in place into the
+ * bf16 hi / lo planes (bit-exact, as ppca_split_f32).  The host buffer must stay valid until the next call
+ * that synchronises the context stream (every ABI call with host outputs does).  Errors: INVALID_ARG for a
+ * NULL pointer or a row range outside the shard; CUDA for a failed copy. */
+ppca_status ppca_upload_rows(ppca_ctx* ctx, const void* host, int64_t rows, int64_t ld_host, const ppca_matrix* X,
+                             int64_t r0);
+
 /* Block power priming (§2.1, multi-component by re-orthonormalisation L63):
  * per iteration Y = X·Wᵀ, Z = YᵀX (fused streaming pass over X), all-reduce, W ← orth(Z)
  * (Q-factor with positive diag R).  W: device [m][d] in/out.  init_seed != 0 initialises W

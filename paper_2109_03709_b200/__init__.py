@@ -30,7 +30,7 @@ EXPORTS = ["ppca_status_string", "ppca_abi_version", "ppca_get_unique_id", "ppca
            "ppca_last_error", "ppca_launch_count", "ppca_generate", "ppca_prime_power", "ppca_prime_oja",
            "ppca_prime_eigengame", "ppca_refine", "ppca_eval", "ppca_captured_variance", "ppca_gram",
            "ppca_philox_words", "ppca_set_pass_impl", "ppca_set_timing", "ppca_get_pass_time",
-           "ppca_last_pass_impl", "ppca_last_power_kernel", "ppca_split_f32", "ppca_get_kernel_time", "ppca_refine_sampled",
+           "ppca_last_pass_impl", "ppca_last_power_kernel", "ppca_split_f32", "ppca_upload_rows", "ppca_get_kernel_time", "ppca_refine_sampled",
            "ppca_check_prop3", "ppca_collective_count", "ppca_experiments_enabled", "ppca_ritz_residuals", "ppca_refine_ex",
            "ppca_check_theorem1", "ppca_set_orth_split"]
 
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
         "ppca_set_timing": (I, [P, I]),
         "ppca_last_pass_impl": (I, [P]),
         "ppca_last_power_kernel": (I, [P]),
+        "ppca_upload_rows": (I, [P, P, I64, I64, ctypes.POINTER(ppca_matrix), I64]),
         "ppca_get_pass_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64)]),
         "ppca_split_f32": (I, [P, P, I64, I64, I64]),
         "ppca_refine_sampled": (I, [P, ctypes.POINTER(ppca_matrix), P, I, I, D, ctypes.c_uint64, P, P,
@@ -302,6 +303,15 @@ def ppca_split_f32(ctx, X, d: int | None = None) -> None:
         raise ValueError("X must be a row-major 2-D tensor")
     _check(ctx, load().ppca_split_f32(ctx, int(X.data_ptr()), X.shape[0], d if d is not None else X.shape[1],
                                       X.stride(0)), "ppca_split_f32")
+
+
+def ppca_upload_rows(ctx, host, X: ppca_matrix, r0: int = 0) -> None:
+    """Copy the rows of the host tensor `host` (row-major 2-D, CPU, fp32 for an fp32 / split X, bf16 for a bf16 X;
+    pinned for an asynchronous copy) into the device shard X at local row r0 (split in place for PPCA_F32_SPLIT)."""
+    if host.dim() != 2 or host.stride(1) != 1 or host.is_cuda:
+        raise ValueError("host must be a row-major 2-D CPU tensor")
+    _check(ctx, load().ppca_upload_rows(ctx, int(host.data_ptr()), host.shape[0], host.stride(0), ctypes.byref(X), r0),
+           "ppca_upload_rows")
 
 
 def ppca_prime_power_ex(ctx, X: ppca_matrix, m: int, iters: int, init_seed: int, W, theta_hist: bool = False,

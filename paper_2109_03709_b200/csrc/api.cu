@@ -462,6 +462,23 @@ ppca_status ppca_split_f32(ppca_ctx* h, void* X, int64_t n_local, int64_t d, int
   return finish(c, "ppca_split_f32");
 }
 
+ppca_status ppca_upload_rows(ppca_ctx* h, const void* host, int64_t rows, int64_t ld_host, const ppca_matrix* X,
+                             int64_t r0) {
+  if (!h || !X || (!host && rows > 0)) return PPCA_ERR_INVALID_ARG;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->device);
+  if (rows < 0 || r0 < 0 || r0 + rows > X->n_local || ld_host < X->d || X->ld < X->d)
+    return set_error(c, PPCA_ERR_INVALID_ARG, "upload rows [%lld, %lld) outside the shard of %lld rows",
+                     (long long)r0, (long long)(r0 + rows), (long long)X->n_local);
+  if (rows == 0) return PPCA_OK;
+  const size_t elt = X->dtype == PPCA_BF16 ? 2 : 4;          // logical element (the split planes are 4 B)
+  uint8_t* dst = static_cast<uint8_t*>(const_cast<void*>(X->data)) + (size_t)r0 * X->ld * elt;
+  PPCA_TRY(check_cuda(c, cudaMemcpy2DAsync(dst, (size_t)X->ld * elt, host, (size_t)ld_host * elt, (size_t)X->d * elt,
+                                           (size_t)rows, cudaMemcpyHostToDevice, c->stream), "upload rows"));
+  if (X->dtype == PPCA_F32_SPLIT) PPCA_TRY(split_f32(c, dst, rows, X->d, X->ld));
+  return finish(c, "ppca_upload_rows");
+}
+
 ppca_status ppca_philox_words(ppca_ctx* h, uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
                               uint32_t* out) {
   if (!h || (!out && count > 0)) return PPCA_ERR_INVALID_ARG;

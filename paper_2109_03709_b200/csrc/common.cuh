@@ -94,6 +94,7 @@ enum Slot {
   S_P3F,                           // Prop. 3 checker stacked vectors [B; T] (fp32)
   S_EPS,                           // power stop rule: W_t copy + column dots
   S_DIST,                          // distributed CholQR: this rank's Z slice and W slice
+  S_SIGN,                          // sign convention partials of very long rows
 };
 
 void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory

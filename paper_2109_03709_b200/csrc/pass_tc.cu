@@ -348,16 +348,6 @@ static ppca_status dispatch_kb(Ctx* c, int mp, const CUtensorMap& tmYT, const CU
   return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: m=%d unsupported", mp);
 }
 
-ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan) {
-  if (!encode_fn()) return set_error(c, PPCA_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
-  if (X->d % 8 != 0 || X->d < 64) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs d %% 8 == 0, d >= 64");
-  if (m > 128 || m < 1) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs m <= 128");
-  if (X->n_local < 128) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs >= 128 local rows");
-  if (reinterpret_cast<uintptr_t>(X->data) % 16) return set_error(c, PPCA_ERR_UNSUPPORTED, "X not 16B aligned");
-  plan->impl = 2;
-  return PPCA_OK;
-}
-
 // TMA maps of X's bf16 planes (box 64 columns × box_rows rows): bf16 X → tmX; split → tmX = hi plane,
 // tmXlo = lo plane (the row stride of a split row is 4·ld bytes = 2·ld bf16)
 static bool make_x_maps(const ppca_matrix* X, uint32_t box_rows, CUtensorMap* hi, CUtensorMap* lo) {
@@ -365,6 +355,23 @@ static bool make_x_maps(const ppca_matrix* X, uint32_t box_rows, CUtensorMap* hi
   const __nv_bfloat16* base = static_cast<const __nv_bfloat16*>(X->data);
   return make_map_bf16(hi, base, X->d, X->n_local, 2 * X->ld, box_rows) &&
          make_map_bf16(lo, base + X->d, X->d, X->n_local, 2 * X->ld, box_rows);
+}
+
+ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan) {
+  if (!encode_fn()) return set_error(c, PPCA_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  if (X->d % 8 != 0 || X->d < 64) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs d %% 8 == 0, d >= 64");
+  if (m > 128 || m < 1) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs m <= 128");
+  if (X->n_local < 1) return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass needs >= 1 local row");
+  if (reinterpret_cast<uintptr_t>(X->data) % 16) return set_error(c, PPCA_ERR_UNSUPPORTED, "X not 16B aligned");
+  if (X->n_local < 128) {
+    // a short shard or minibatch window (the last block of a schedule): one partial tile whose rows beyond
+    // n_local the TMA fills with zeros — if the driver accepts a 128-row box over fewer rows
+    CUtensorMap probe, probe_lo;
+    if (X->dtype == PPCA_F32 || !make_x_maps(X, 128, &probe, &probe_lo))
+      return set_error(c, PPCA_ERR_UNSUPPORTED, "tcgen05 pass: %lld rows do not fill a TMA tile", (long long)X->n_local);
+  }
+  plan->impl = 2;
+  return PPCA_OK;
 }
 
 // W' (bf16 + its fp32 value copy) → S_TC1;  returns pointers

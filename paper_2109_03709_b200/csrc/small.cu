@@ -985,10 +985,70 @@ __global__ void sign_rows_kernel(float* __restrict__ E, int64_t d) {
     for (int64_t x = threadIdx.x; x < d; x += blockDim.x) row[x] = -row[x];
 }
 
+// Very long rows (d ≥ 2^20, the huge-d regime): one block per row would stream megabytes alone, so the rows are
+// cut into ROWSLICES slices — partial (|max|, index) per slice, then every slice block reduces its row's partials
+// (ties → lower index, so the order does not matter) and flips its slice.  Shorter rows keep sign_rows_kernel.
+constexpr int64_t kLongRow = int64_t(1) << 20;
+constexpr int ROWSLICES = 64;
+__global__ void sign_part_kernel(const float* __restrict__ E, int64_t d, float* __restrict__ pb,
+                                 long long* __restrict__ pi) {
+  const int64_t L = (d + ROWSLICES - 1) / ROWSLICES, x0 = blockIdx.x * L, x1 = min(d, x0 + L);
+  const float* row = E + (int64_t)blockIdx.y * d;
+  float best = -1.f;
+  long long bi = x0;
+  for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
+    const float a = fabsf(row[x]);
+    if (a > best) { best = a; bi = x; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  __shared__ float sb[32];
+  __shared__ long long si[32];
+  if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < bi)) { best = sb[w]; bi = si[w]; }
+    pb[blockIdx.y * ROWSLICES + blockIdx.x] = best;
+    pi[blockIdx.y * ROWSLICES + blockIdx.x] = bi;
+  }
+}
+__global__ void sign_apply_kernel(float* __restrict__ E, int64_t d, const float* __restrict__ pb,
+                                  const long long* __restrict__ pi) {
+  __shared__ float sgn;
+  float* row = E + (int64_t)blockIdx.y * d;
+  if (threadIdx.x == 0) {
+    float b = pb[blockIdx.y * ROWSLICES];
+    long long i = pi[blockIdx.y * ROWSLICES];
+    for (int s = 1; s < ROWSLICES; ++s) {
+      const float ob = pb[blockIdx.y * ROWSLICES + s];
+      const long long oi = pi[blockIdx.y * ROWSLICES + s];
+      if (ob > b || (ob == b && oi < i)) { b = ob; i = oi; }
+    }
+    sgn = row[i] < 0.f ? -1.f : 1.f;
+  }
+  __syncthreads();
+  const int64_t L = (d + ROWSLICES - 1) / ROWSLICES, x0 = blockIdx.x * L, x1 = min(d, x0 + L);
+  if (sgn < 0.f)
+    for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) row[x] = -row[x];
+}
+
 ppca_status lift_rows(Ctx* c, const double* R, int ldr, const float* W, int m, int k, int64_t d, float* E,
                       bool apply_sign, cudaStream_t stream) {
   PPCA_TRY(apply_rows(c, R, ldr, k, m, nullptr, false, W, d, E, stream));
-  if (apply_sign) {
+  if (apply_sign && d >= kLongRow) {
+    uint8_t* buf = (uint8_t*)scratch(c, S_SIGN, (size_t)k * ROWSLICES * (sizeof(float) + sizeof(long long)));
+    if (!buf) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    long long* pi = reinterpret_cast<long long*>(buf);
+    float* pb = reinterpret_cast<float*>(pi + (size_t)k * ROWSLICES);
+    sign_part_kernel<<<dim3(ROWSLICES, k), 256, 0, stream>>>(E, d, pb, pi);
+    PPCA_LAUNCH_CHECK(c, "sign_part");
+    sign_apply_kernel<<<dim3(ROWSLICES, k), 256, 0, stream>>>(E, d, pb, pi);
+    PPCA_LAUNCH_CHECK(c, "sign_apply");
+  } else if (apply_sign) {
     sign_rows_kernel<<<k, 256, 0, stream>>>(E, d);
     PPCA_LAUNCH_CHECK(c, "sign_rows");
   }
@@ -1031,9 +1091,41 @@ __global__ void scale_rows_kernel(float* __restrict__ W, int m, int64_t d, const
   W[e] = (float)v;
 }
 
+// long rows (d ≥ 2^20): partial squared norms per slice, summed in slice order
+__global__ void row_norm_part_kernel(const float* __restrict__ W, int64_t d, double* __restrict__ part) {
+  const int64_t L = (d + ROWSLICES - 1) / ROWSLICES, x0 = blockIdx.x * L, x1 = min(d, x0 + L);
+  const float* row = W + (int64_t)blockIdx.y * d;
+  double s = 0.0;
+  for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) s += (double)row[x] * row[x];
+  s = warp_sum(s);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.y * ROWSLICES + blockIdx.x] = t;
+  }
+}
+__global__ void row_norm_finish_kernel(const double* __restrict__ part, int m, double* __restrict__ nrm) {
+  const int j = threadIdx.x;
+  if (j >= m) return;
+  double t = 0.0;
+  for (int s = 0; s < ROWSLICES; ++s) t += part[j * ROWSLICES + s];
+  nrm[j] = sqrt(t);
+}
+
 ppca_status normalize_rows(Ctx* c, float* W, int m, int64_t d) {
-  double* nrm = (double*)scratch(c, S_ROWRED, (size_t)PPCA_MAX_M * sizeof(double));
-  row_norm_kernel<<<m, 256, 0, c->stream>>>(W, d, nrm);
+  double* nrm = (double*)scratch(c, S_ROWRED, (size_t)PPCA_MAX_M * (ROWSLICES + 1) * sizeof(double));
+  if (!nrm) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  if (d >= kLongRow) {
+    double* part = nrm + PPCA_MAX_M;
+    row_norm_part_kernel<<<dim3(ROWSLICES, m), 256, 0, c->stream>>>(W, d, part);
+    PPCA_LAUNCH_CHECK(c, "row_norm_part");
+    row_norm_finish_kernel<<<1, 128, 0, c->stream>>>(part, m, nrm);
+  } else {
+    row_norm_kernel<<<m, 256, 0, c->stream>>>(W, d, nrm);
+  }
   PPCA_LAUNCH_CHECK(c, "row_norm");
   scale_rows_kernel<<<(unsigned)ceil_div((int64_t)m * d, 256), 256, 0, c->stream>>>(W, m, d, nrm, c->d_err);
   PPCA_LAUNCH_CHECK(c, "scale_rows");
@@ -1192,7 +1284,11 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
     if (lane == 0) twoU[j] = 2.0 * (ajj - part);
   }
   __syncthreads();
-  // update per column chunk
+  // update per column chunk; the squared row norms of this CTA's chunks accumulate in chunk order (lane 0 of
+  // the row's warp) and leave as one partial per CTA
+  double racc[PPCA_MAX_M / 8];
+#pragma unroll
+  for (int q = 0; q < PPCA_MAX_M / 8; ++q) racc[q] = 0.0;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t x0 = ch * EG_XC;
     copy_batched<8>(tid, (int64_t)m * EG_XC, blockDim.x,
@@ -1244,19 +1340,26 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
         sq = (double)wf * wf;
       }
       sq = warp_sum(sq);
-      if (lane == 0) rowpart[ch * m + j] = sq;
+      racc[q] += sq;
     }
     __syncthreads();
   }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+      const int j = warp + q * nw;
+      if (j < m) rowpart[(int64_t)blockIdx.x * m + j] = racc[q];
+    }
+  }
   grid.sync();
-  // row norms: thread (row j, slice s) sums chunks c ≡ s (mod ns) in order (8 loads in flight), the slices
+  // row norms: thread (row j, slice s) sums the CTA partials c ≡ s (mod ns) in order (8 loads in flight), the slices
   // are added in slice order — the same sums in every CTA; then this CTA's columns are rescaled
   {
     const int ns = (int)blockDim.x / m;                   // ≥ 2 for m ≤ 128
     const int j = threadIdx.x % m, sl = threadIdx.x / m;
     double* part = reinterpret_cast<double*>(mvs);        // ns × m (the MV slab is free now)
     if (sl < ns)
-      part[sl * m + j] = sum_in_order<8>(sl, nchunks, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
+      part[sl * m + j] = sum_in_order<8>(sl, (int64_t)gridDim.x, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
     __syncthreads();
     if (threadIdx.x < m) {
       double s2 = 0.0;
@@ -1301,12 +1404,12 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
     cudaGetLastError();
     return false;
   }
-  double* rowpart = (double*)scratch(c, S_ROWRED, (size_t)nchunks * m * sizeof(double));
+  const int grid = (int)std::min<int64_t>(nchunks, (int64_t)per_sm * c->sm_count);
+  double* rowpart = (double*)scratch(c, S_ROWRED, (size_t)grid * m * sizeof(double));   // one partial per CTA
   if (!rowpart) {
     *st = set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
     return true;
   }
-  const int grid = (int)std::min<int64_t>(nchunks, (int64_t)per_sm * c->sm_count);
   void* args[] = {(void*)&MV, (void*)&A, (void*)&V, (void*)&vel, (void*)&m, (void*)&d, (void*)&alpha, (void*)&mu,
                   (void*)&rowpart, (void*)&c->d_err};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)eg_update_kernel, grid, 256, args, smem, c->stream);

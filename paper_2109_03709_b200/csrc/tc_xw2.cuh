@@ -45,8 +45,10 @@ struct Cfg {
   // W' stages: a 2·MP-row W' chunk is as large as (MP = 64) or twice (MP = 128) the X chunk it multiplies and
   // comes from L2, so its ring must cover L2 latency too (measured on C5: 2 stages starve the MMA)
   // PAIR (2-CTA UMMA, M = 256): each CTA of the pair holds half of every W' chunk (NB/2 rows)
-  static constexpr int NWS = PAIR ? 4 : (MP <= 64 ? 4 : (XM == 1 ? 3 : 2));
+  // small m: the W' chunk is only 2·MP rows (4 KB at MP = 16) and, at huge d (W' beyond L2), comes from HBM, so
+  // the ring keeps ≥ 64 KB in flight (up to 16 stages) instead of 4 stages
   static constexpr uint32_t WST = (PAIR ? NB / 2 : NB) * 128;
+  static constexpr int NWS = PAIR ? 4 : (MP < 64 ? (int)(65536 / WST > 16 ? 16 : 65536 / WST) : (MP == 64 ? 4 : (XM == 1 ? 3 : 2)));
   // fp32 Y rows for the CUDA-core S (the tensor-core S keeps the segment sums in registers)
   static constexpr size_t YS = SMMA ? 0 : (size_t)BM * (MP + 4) * 4;
   static constexpr size_t YSM = SMMA ? (size_t)2 * YBLK : 0;    // bf16 [Y_hi | Y_lo] operand tile

@@ -564,3 +564,25 @@ def test_distributed_orth_emulated_slices_match(P, ctx, blocks):
     _, S_hist = O.prime_power(X64, G.init_gaussians(w.init_seed, w.m, s.d), 4)
     for t in range(4):
         assert U.ritz_rel_err(th1[t], O.ritz_values(S_hist[t])) < 1e-3
+
+
+def test_upload_rows_matches_device_split(P, ctx):
+    """ppca_upload_rows (the e2e path: host rows → the device shard, split in place) equals the device-side
+    ppca_split_f32 of the same rows bit for bit, for a row block at an offset, and for bf16 rows."""
+    import torch
+    rng = np.random.default_rng(7)
+    n, d = 3001, 256
+    host = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).pin_memory()
+    ref = host.cuda()
+    P.ppca_split_f32(ctx, ref, d)
+    dev = torch.zeros((n, d), dtype=torch.float32, device="cuda")
+    Xm = P.matrix(dev, split=True)
+    P.ppca_upload_rows(ctx, host[:1000], Xm, 0)
+    P.ppca_upload_rows(ctx, host[1000:], Xm, 1000)
+    assert torch.equal(dev.view(torch.int32), ref.view(torch.int32))
+    hb = host.to(torch.bfloat16)
+    devb = torch.zeros((n, d), dtype=torch.bfloat16, device="cuda")
+    P.ppca_upload_rows(ctx, hb, P.matrix(devb), 0)
+    assert torch.equal(devb.cpu().view(torch.int16), hb.view(torch.int16))
+    with pytest.raises(P.PPCAError):
+        P.ppca_upload_rows(ctx, host[:10], Xm, n - 5)          # outside the shard
