@@ -17,6 +17,17 @@ struct ppca_ctx {
 
 namespace ppca {
 
+int g_pdl = tune_env("PPCA_PDL", 1);
+
+// ABI entry: select the device and order the library stream after the caller's stream
+static void enter(Ctx* c) {
+  cudaSetDevice(c->device);
+  if (c->own_stream) {
+    cudaEventRecord(c->fork_ev, c->user_stream);
+    cudaStreamWaitEvent(c->stream, c->fork_ev, 0);
+  }
+}
+
 ppca_status generate(Ctx* c, const ppca_gen_spec* s, void* X, int64_t ld, int64_t* n_local_out, double* mu_host);
 ppca_status philox_words(Ctx* c, uint64_t seed, uint32_t stream, uint64_t first, int64_t count, uint32_t* out);
 ppca_status split_f32(Ctx* c, void* X, int64_t n_local, int64_t d, int64_t ld);
@@ -340,8 +351,23 @@ ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank,
   c->rank = rank;
   c->world = world;
   c->sm_count = prop.multiProcessorCount;
-  c->stream = (cudaStream_t)stream;
-  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+  c->user_stream = (cudaStream_t)stream;
+  c->stream = c->user_stream;
+  // the library's own stream at the highest priority, the side stream (off-critical-path Ritz solves and
+  // operand Grams) at the lowest: when both have CTAs waiting, the critical path's are dispatched first.
+  // Every call orders the library stream after the caller's (enter()) and returns once its work is done.
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  static const int use_prio = tune_env("PPCA_PRIO", 1);
+  if (use_prio && prio_hi != prio_lo) {
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
+      delete h;
+      return PPCA_ERR_CUDA;
+    }
+    c->own_stream = true;
+  }
+  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&c->d_err, sizeof(int)) != cudaSuccess || cudaMemset(c->d_err, 0, sizeof(int)) != cudaSuccess) {
@@ -373,7 +399,7 @@ ppca_status ppca_ctx_create(int device, void* stream, const void* uid, int rank,
 ppca_status ppca_ctx_destroy(ppca_ctx* h) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   cudaStreamSynchronize(c->stream);
   if (c->side) cudaStreamSynchronize(c->side);
   for (int i = 0; i < Ctx::kSlots; ++i)
@@ -383,6 +409,8 @@ ppca_status ppca_ctx_destroy(ppca_ctx* h) {
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->nccl_comm) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
   pass_release(c);
   delete h;
@@ -422,13 +450,13 @@ ppca_status ppca_set_timing(ppca_ctx* h, int enable) {
 
 ppca_status ppca_get_pass_time(ppca_ctx* h, double* ms_total, int64_t* passes) {
   if (!h || !ms_total || !passes) return PPCA_ERR_INVALID_ARG;
-  cudaSetDevice(h->c.device);
+  enter(&h->c);
   return pass_time_collect(&h->c, ms_total, passes);
 }
 
 ppca_status ppca_get_kernel_time(ppca_ctx* h, int which, double* ms_total, int64_t* launches) {
   if (!h || !ms_total || !launches || which < 0 || which > 1) return PPCA_ERR_INVALID_ARG;
-  cudaSetDevice(h->c.device);
+  enter(&h->c);
   return kernel_time_collect(&h->c, which, ms_total, launches);
 }
 
@@ -449,7 +477,7 @@ ppca_status ppca_generate(ppca_ctx* h, const ppca_gen_spec* spec, void* X, int64
                           double* col_mean_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(generate(c, spec, X, ld, n_local_out, col_mean_host));
   return finish(c, "ppca_generate");
 }
@@ -457,7 +485,7 @@ ppca_status ppca_generate(ppca_ctx* h, const ppca_gen_spec* spec, void* X, int64
 ppca_status ppca_split_f32(ppca_ctx* h, void* X, int64_t n_local, int64_t d, int64_t ld) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(split_f32(c, X, n_local, d, ld));
   return finish(c, "ppca_split_f32");
 }
@@ -466,7 +494,7 @@ ppca_status ppca_upload_rows(ppca_ctx* h, const void* host, int64_t rows, int64_
                              int64_t r0) {
   if (!h || !X || (!host && rows > 0)) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   if (rows < 0 || r0 < 0 || r0 + rows > X->n_local || ld_host < X->d || X->ld < X->d)
     return set_error(c, PPCA_ERR_INVALID_ARG, "upload rows [%lld, %lld) outside the shard of %lld rows",
                      (long long)r0, (long long)(r0 + rows), (long long)X->n_local);
@@ -483,7 +511,7 @@ ppca_status ppca_philox_words(ppca_ctx* h, uint64_t seed, uint32_t stream, uint6
                               uint32_t* out) {
   if (!h || (!out && count > 0)) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(philox_words(c, seed, stream, first, count, out));
   return finish(c, "ppca_philox_words");
 }
@@ -493,7 +521,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
                              float* W, double* theta_hist_host, int* iters_done) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   if (iters_done) *iters_done = 0;
   PPCA_TRY(check_matrix(c, X, m));
   if (!W || iters < 0 || !(eps == eps)) return set_error(c, PPCA_ERR_INVALID_ARG, "null W, iters < 0 or NaN eps");
@@ -696,7 +724,7 @@ ppca_status ppca_prime_oja(ppca_ctx* h, const ppca_matrix* X, int m, int batch, 
                            int64_t steps, uint64_t init_seed, float* W, float* velocity, int64_t* step_io) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(minibatch_common(c, X, m, batch, steps, init_seed, W, velocity, step_io, false, alpha, momentum));
   return finish(c, "ppca_prime_oja");
 }
@@ -705,7 +733,7 @@ ppca_status ppca_prime_eigengame(ppca_ctx* h, const ppca_matrix* X, int m, int b
                                  int64_t steps, uint64_t init_seed, float* V, float* velocity, int64_t* step_io) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(minibatch_common(c, X, m, batch, steps, init_seed, V, velocity, step_io, true, alpha, momentum));
   return finish(c, "ppca_prime_eigengame");
 }
@@ -807,7 +835,7 @@ static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int
 ppca_status ppca_refine(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, int k, float* E, double* theta_host,
                         int* subspace_dim) {
   if (!h) return PPCA_ERR_INVALID_ARG;
-  cudaSetDevice(h->c.device);
+  enter(&h->c);
   return refine_impl(&h->c, X, V, m, k, 1.0, 0, E, theta_host, subspace_dim, nullptr);
 }
 
@@ -815,7 +843,7 @@ ppca_status ppca_refine_ex(ppca_ctx* h, const ppca_matrix* X, const float* V, in
                            double* theta_host, int* subspace_dim) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   if (flags & ~(unsigned)PPCA_REFINE_ORTHONORMAL) return set_error(&h->c, PPCA_ERR_INVALID_ARG, "unknown refine flags");
-  cudaSetDevice(h->c.device);
+  enter(&h->c);
   return refine_impl(&h->c, X, V, m, k, 1.0, 0, E, theta_host, subspace_dim, nullptr, flags);
 }
 
@@ -823,7 +851,7 @@ ppca_status ppca_refine_sampled(ppca_ctx* h, const ppca_matrix* X, const float* 
                                 uint64_t sample_seed, float* E, double* theta_host, int* subspace_dim,
                                 int64_t* rows_used) {
   if (!h) return PPCA_ERR_INVALID_ARG;
-  cudaSetDevice(h->c.device);
+  enter(&h->c);
   return refine_impl(&h->c, X, V, m, k, fraction, sample_seed, E, theta_host, subspace_dim, rows_used);
 }
 
@@ -835,7 +863,7 @@ ppca_status ppca_check_prop3(ppca_ctx* h, const ppca_matrix* X, const float* V, 
                              double tol, double* angles_host, int* flags_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(check_matrix(c, X, m));
   if (!V || !T || !angles_host || !flags_host || upto < 1 || upto > PPCA_MAX_M || !(tol >= 0.0))
     return set_error(c, PPCA_ERR_INVALID_ARG, "bad check_prop3 args (upto=%d)", upto);
@@ -883,7 +911,7 @@ ppca_status ppca_check_theorem1(ppca_ctx* h, const ppca_matrix* X, const float* 
                                 int* holds_out) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   if (!V || !T || !upto_out || !ang_priming_host || !ang_ppca_host || !holds_out || k < 1 || k > m || !(tol >= 0.0))
     return set_error(c, PPCA_ERR_INVALID_ARG, "bad check_theorem1 args (k=%d, m=%d)", k, m);
   std::vector<double> cang(k);
@@ -925,7 +953,7 @@ ppca_status ppca_eval(ppca_ctx* h, const float* E, const float* T, int k, int64_
                       double* angles_host, int* lces_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   if (!E || !T || k < 1 || d < 1 || (nthr > 0 && (!thr_host || !lces_host)))
     return set_error(c, PPCA_ERR_INVALID_ARG, "bad eval args");
   double* dots = (double*)scratch(c, S_ROWRED, (size_t)std::max(k, PPCA_MAX_M) * sizeof(double));
@@ -950,7 +978,7 @@ ppca_status ppca_ritz_residuals(ppca_ctx* h, const ppca_matrix* X, const float* 
                                 double* res_host, double* res_gram_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(check_matrix(c, X, k));
   if (!E || !theta_host || !res_host) return set_error(c, PPCA_ERR_INVALID_ARG, "null E / theta / res");
   const int64_t d = X->d;
@@ -986,7 +1014,7 @@ ppca_status ppca_ritz_residuals(ppca_ctx* h, const ppca_matrix* X, const float* 
 ppca_status ppca_captured_variance(ppca_ctx* h, const ppca_matrix* X, const float* V, int m, double* var_host) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(check_matrix(c, X, m));
   if (!V || !var_host) return set_error(c, PPCA_ERR_INVALID_ARG, "null V / output");
   double* S = (double*)scratch(c, S_S, (size_t)m * m * sizeof(double));
@@ -1005,7 +1033,7 @@ ppca_status ppca_captured_variance(ppca_ctx* h, const ppca_matrix* X, const floa
 ppca_status ppca_gram(ppca_ctx* h, const ppca_matrix* X, double* G) {
   if (!h) return PPCA_ERR_INVALID_ARG;
   Ctx* c = &h->c;
-  cudaSetDevice(c->device);
+  enter(c);
   PPCA_TRY(check_matrix(c, X, 1));
   if (!G) return set_error(c, PPCA_ERR_INVALID_ARG, "null G");
   const int64_t d = X->d;

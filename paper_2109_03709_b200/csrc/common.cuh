@@ -30,7 +30,10 @@ typedef ppca_status (*AllreduceFn)(Ctx*, void* buf, size_t count, int is_f64);
 struct Ctx {
   int device = 0;
   int rank = 0, world = 1;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the library's stream (own high-priority stream, or the caller's)
+  cudaStream_t user_stream = nullptr; // the caller's stream (ppca_ctx_create)
+  bool own_stream = false;
+  cudaEvent_t fork_ev = nullptr;      // caller's stream → library stream at every ABI entry
   cudaStream_t side = nullptr;        // side stream (Ritz solves overlap the next pass)
   cudaEvent_t prep_ev = nullptr;     // when set: recorded once the pass operand W' is prepared (power loop)
   // deferred S reduction of the fused pass (power loop with θ history on one GPU: S feeds only the side-stream
@@ -129,6 +132,39 @@ static inline int tune_env(const char* name, int dflt) {
   (void)name;
   return dflt;
 #endif
+}
+
+// ----------------------------------------------------------------------------- programmatic dependent launch
+// The m×m chain between two passes is a row of short dependent kernels; with stream serialisation each one
+// starts only after its predecessor has drained, so every boundary costs a launch latency.  The chain kernels
+// are launched with programmatic stream serialisation instead: the dependent grid may become resident while
+// its predecessor still runs and blocks in pdl_wait() (griddepcontrol.wait: returns once every prerequisite
+// grid has completed and its memory is visible) before it touches global memory; each kernel calls
+// pdl_trigger() right after its own wait, so at most one grid waits behind a running one.  Both instructions
+// are no-ops in a grid launched without the attribute, so every kernel may carry them.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+extern int g_pdl;   // 1: chain kernels use programmatic dependent launch (experiment builds: PPCA_PDL=0 turns it off)
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 // cudaFuncSetAttribute (dynamic shared memory opt-in) belongs to each device's context: call sites keep a

@@ -277,6 +277,7 @@ __global__ void reduce_splits_f32_kernel(const double* __restrict__ P, int nspli
 // output summing every split waited nsplit/8 dependent round trips (128 splits: 14 µs).
 __global__ void __launch_bounds__(256) reduce_splits_f64_kernel(const double* __restrict__ P, int nsplit, int64_t count,
                                                                 double* __restrict__ out) {
+  pdl_enter();
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + lane;
@@ -307,7 +308,7 @@ ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_
 ppca_status launch_reduce_splits_f64(Ctx* c, const double* P, int nsplit, int64_t count, double* out,
                                      cudaStream_t st) {
   if (count <= 0) return PPCA_OK;
-  reduce_splits_f64_kernel<<<(unsigned)ceil_div(count, (int64_t)32), 256, 0, st>>>(P, nsplit, count, out);
+  launch_pdl(reduce_splits_f64_kernel, dim3((unsigned)ceil_div(count, (int64_t)32)), dim3(256), 0, st, P, nsplit, count, out);
   PPCA_LAUNCH_CHECK(c, "reduce_splits_f64");
   return PPCA_OK;
 }

@@ -90,6 +90,7 @@ __device__ __forceinline__ float4 ldg_x4(const float* __restrict__ X, int64_t ld
 // four consecutive elements per thread (d % 8 == 0 on the tensor-core path): 16-byte loads / stores
 __global__ void prep_w_kernel(const float* __restrict__ W, int m, int mp, int64_t d, __nv_bfloat16* __restrict__ Wb,
                               float* __restrict__ Wr) {
+  pdl_enter();
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e >= (int64_t)mp * d) return;
   const int64_t i = e / d;
@@ -115,6 +116,7 @@ __global__ void prep_w_kernel(const float* __restrict__ W, int m, int mp, int64_
 // added in warp order — a fixed order, so the result is deterministic.
 __global__ void __launch_bounds__(256) reduce_spart_kernel(const double* __restrict__ Spart, int nparts, int mp, int m,
                                                            double* __restrict__ S) {
+  pdl_enter();
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(256) reduce_spart_kernel(const double* __restr
 // (S partials of the tensor-core S: rows a and a+mp hold the hi- and lo-row halves of D; fixed order)
 __global__ void __launch_bounds__(256) reduce_spart2_kernel(const double* __restrict__ Spart, int nparts, int mp,
                                                             int m, double* __restrict__ S) {
+  pdl_enter();
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
@@ -180,6 +183,7 @@ __device__ __forceinline__ int64_t z_index(int j, int64_t x, int m, int64_t ds) 
 
 __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
                                                              int mp, int m, int64_t d, float* __restrict__ Z, int64_t ds) {
+  pdl_enter();
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t x = blockIdx.x;
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __rest
 // fp64; a block covers 256·4/mp columns and leaves through shared memory as runs of Z's rows.
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z, int64_t ds) {
+  pdl_enter();
   __shared__ float tr[128][65];
   const int tpc = mp >> 2;                           // threads per column (mp ≤ 128, multiple of 16)
   const int cpb = 256 / tpc;                         // columns per block (≤ 64)
@@ -234,10 +239,10 @@ __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict_
 static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z) {
   const int64_t ds = c->z_block_cols > 0 ? c->z_block_cols : d;
   if (nrg > 16)
-    reduce_zp_cols_kernel<<<dim3((unsigned)d, (unsigned)ceil_div(m, 32)), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z,
+    launch_pdl(reduce_zp_cols_kernel, dim3(dim3((unsigned)d, (unsigned)ceil_div(m, 32))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z,
                                                                                             ds);
   else
-    reduce_zp_kernel<<<(unsigned)ceil_div(d, (int64_t)(256 / (mp / 4))), 256, 0, c->stream>>>(Zp, nrg, dpad, mp, m, d, Z, ds);
+    launch_pdl(reduce_zp_kernel, dim3((unsigned)ceil_div(d, (int64_t)(256 / (mp / 4)))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
 }
 
 // ============================================================================ host side
@@ -250,6 +255,35 @@ static int pad16(int m) { return (m + 15) & ~15; }
 // one CTA per SM; one SM is left free while side-stream work (the Ritz solve of the previous
 // iterate) may be resident, otherwise the CTA queued behind it delays the whole persistent pass
 static int persistent_ctas(const Ctx* c) { return c->side_busy ? c->sm_count - 1 : c->sm_count; }
+
+// How many 2-CTA clusters of a kernel (dynamic smem, threads) can be resident at once; cached per device in
+// *cache.  The persistent pair kernels deal tiles statically, so a cluster beyond that number would start only
+// when another has finished its whole share: launching more than fit doubles the tail (not every one of the
+// 148 SMs can pair up; C3: 74 clusters 1.02-1.05 ms, 73 clusters 0.885 ms).
+static int max_pair_clusters(Ctx* c, const void* kern, size_t smem, int threads, int* cache) {
+  const int dev = c->device & 63;
+  if (cache[dev] > 0) return cache[dev];
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * (c->sm_count / 2)));
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = c->sm_count / 2;
+  }
+  cache[dev] = n;
+  return n;
+}
 
 template <int MP, int XM>
 static ppca_status launch_ka(Ctx* c, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmXlo,
@@ -268,7 +302,7 @@ static ppca_status launch_kb(Ctx* c, const CUtensorMap& tmYT, const CUtensorMap&
   const size_t smem = kb::Cfg<MP, XLO, LEAN>::SMEM;
   auto kern = xty_tc_kernel<MP, XBF16, XLO, LEAN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kb::NTHREADS, smem, c->stream>>>(tmYT, tmX, tmXlo, bp);
+  launch_pdl(kern, dim3(grid), dim3(kb::NTHREADS), smem, c->stream, tmYT, tmX, tmXlo, bp);
   PPCA_LAUNCH_CHECK(c, "xty_tc_kernel");
   return PPCA_OK;
 }
@@ -280,20 +314,22 @@ static ppca_status launch_ka2(Ctx* c, const CUtensorMap& tmW, const CUtensorMap&
   auto kern = xw_tma_kernel<MP, XM, PAIR>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if constexpr (!PAIR) {
-    kern<<<grid, ka2::NTHREADS, smem, c->stream>>>(tmW, tmX, tmXlo, kp);
+    launch_pdl(kern, dim3(grid), dim3(ka2::NTHREADS), smem, c->stream, tmW, tmX, tmXlo, kp);
   } else {                                          // CTA pairs: clusters of 2
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(ka2::NTHREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = g_pdl ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmXlo, kp);
   }
   PPCA_LAUNCH_CHECK(c, "xw_tma_kernel");
@@ -380,7 +416,7 @@ static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv
   if (!buf) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   *Wb = reinterpret_cast<__nv_bfloat16*>(buf);
   *Wr = reinterpret_cast<float*>(buf + (((size_t)2 * mp * d * 2 + 255) & ~(size_t)255));
-  prep_w_kernel<<<(unsigned)ceil_div((int64_t)mp * d, 1024), 256, 0, c->stream>>>(W, m, mp, d, *Wb, *Wr);
+  launch_pdl(prep_w_kernel, dim3((unsigned)ceil_div((int64_t)mp * d, 1024)), dim3(256), 0, c->stream, W, m, mp, d, *Wb, *Wr);
   PPCA_LAUNCH_CHECK(c, "prep_w");
   return PPCA_OK;
 }
@@ -412,7 +448,13 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   if (dbg < 0) dbg = tune_env("PPCA_DBG", 0);
   kp.dbg = dbg;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c), kp.ntiles * ksplit));
-  if (pair) grid = (int)std::max<int64_t>(2, std::min<int64_t>(persistent_ctas(c) & ~1, 2 * ((kp.ntiles + 1) / 2)));
+  if (pair) {
+    static int cache[64] = {};
+    const int maxc = max_pair_clusters(c, (const void*)xw_tma_kernel<128, 1, true>, ka2::Cfg<128, 1, true>::SMEM,
+                                       ka2::NTHREADS, cache);
+    grid = (int)std::max<int64_t>(2, std::min<int64_t>(std::min(persistent_ctas(c) & ~1, 2 * maxc),
+                                                       2 * ((kp.ntiles + 1) / 2)));
+  }
   // TMA-staged X (bf16, split) runs kernel A2; its S partial has 2·mp rows when S is on the tensor cores
   const bool tma_x = X->dtype != PPCA_F32;
   const bool smma = tma_x && mp == 64;
@@ -427,9 +469,9 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
   kernel_timer_mark(c, 0);
   if (ksplit > 1) return PPCA_OK;                 // partial Y out; the caller forms S from the summed Y
   if (smma)
-    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    launch_pdl(reduce_spart2_kernel, dim3((unsigned)ceil_div(m * m, 32)), dim3(256), 0, c->stream, Spart, grid, mp, m, S);
   else
-    reduce_spart_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    launch_pdl(reduce_spart_kernel, dim3((unsigned)ceil_div(m * m, 32)), dim3(256), 0, c->stream, Spart, grid, mp, m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
   return PPCA_OK;
 }
@@ -442,6 +484,7 @@ constexpr int YS_RB = 32;
 __global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Ypart, int ksplit, int64_t n, int mp,
                                                      int m, __nv_bfloat16* __restrict__ YT, int64_t ldyt,
                                                      double* __restrict__ Spart) {
+  pdl_enter();
   extern __shared__ float ysm[];                      // YS_RB × (mp + 1)
   const int ld = mp + 1;
   const int64_t r0 = (int64_t)blockIdx.x * YS_RB;
@@ -548,7 +591,7 @@ ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, con
   if (plan->tiles_dev)                          // rows outside the sample stay zero in every part
     PPCA_TRY(check_cuda(c, cudaMemsetAsync(Ypart, 0, (size_t)ksplit * n * mp * sizeof(float), c->stream), "zero Y"));
   PPCA_TRY(run_ka(c, X, Wb, m, mp, S, nullptr, 0, ksplit, Ypart, plan->tiles_dev, plan->ntiles_sel));
-  ysum_s_kernel<<<(unsigned)nb, 256, (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream>>>(Ypart, ksplit, n, mp, m,
+  launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream, Ypart, ksplit, n, mp, m,
                                                                                             nullptr, 0, Sp);
   PPCA_LAUNCH_CHECK(c, "ysum_s");
   return launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S);
@@ -701,7 +744,7 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
     c->s_mp = mp;
     c->s_m = m;
   } else {
-    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    launch_pdl(reduce_spart2_kernel, dim3((unsigned)ceil_div(m * m, 32)), dim3(256), 0, c->stream, Spart, grid, mp, m, S);
     PPCA_LAUNCH_CHECK(c, "reduce_spart");
   }
   launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
@@ -729,14 +772,35 @@ static cudaError_t launch_pair(Ctx* c, int grid, const CUtensorMap& tmW, const C
   cfg.blockDim = dim3(kp2::NTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // its prologue overlaps prep_w's tail
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, tmW, tmX, tmXlo, tmXb, pp);
+}
+
+template <int XM, int NSTA, int NWS, int NSTB, int KR>
+static int pair_max_clusters(Ctx* c) {
+  static int cache[64] = {};
+  return max_pair_clusters(c, (const void*)xwz_pair_kernel<XM, NSTA, NWS, NSTB, KR>,
+                           pair_smem<XM, NSTA, NWS, NSTB, KR>(), kp2::NTHREADS, cache);
+}
+
+template <int XM>
+static int pair_max_clusters_cfg(Ctx* c, int cfg) {
+  switch (cfg) {
+    case 1: return pair_max_clusters<XM, 2, 2, 2, 32>(c);
+    case 2: return pair_max_clusters<XM, 2, 2, 3, 16>(c);
+    case 3: return pair_max_clusters<XM, 2, 3, 3, 16>(c);
+    case 4: return pair_max_clusters<XM, 3, 1, 3, 16>(c);
+    case 5: return pair_max_clusters<XM, 2, 2, 4, 16>(c);
+    default: return pair_max_clusters<XM, 3, 2, 2, 16>(c);
+  }
 }
 
 template <int XM>
@@ -763,7 +827,13 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
   const int mp = 64;
   const int64_t n = X->n_local, d = X->d;
   const int64_t ntiles = ceil_div(n, kp2::BM);
-  int nrg = (int)std::max<int64_t>(1, std::min<int64_t>(persistent_ctas(c) / 2, ntiles));
+  static int cfg = -1;
+  if (cfg < 0) cfg = tune_env("PPCA_PAIR_CFG", 0);
+  const int maxc = X->dtype == PPCA_F32_SPLIT ? pair_max_clusters_cfg<2>(c, cfg) : pair_max_clusters_cfg<1>(c, cfg);
+  static int nrg_cap = -1;                        // PPCA_PAIR_NRG (experiment builds): cap the cluster count
+  if (nrg_cap < 0) nrg_cap = tune_env("PPCA_PAIR_NRG", 0);
+  int nrg = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(persistent_ctas(c) / 2, maxc), ntiles));
+  if (nrg_cap > 0) nrg = std::min(nrg, nrg_cap);
   const int64_t tpr = ceil_div(ntiles, (int64_t)nrg);
   nrg = (int)ceil_div(ntiles, tpr);
   const int grid = 2 * nrg;
@@ -774,8 +844,6 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
   CUtensorMap tmW, tmX, tmXlo, tmXb, tmXblo;
   if (!make_map_bf16(&tmW, Wb, d, 2 * mp, d, 2 * mp)) return set_error(c, PPCA_ERR_CUDA, "tensor map W failed");
   tmXlo = tmW;
-  static int cfg = -1;
-  if (cfg < 0) cfg = tune_env("PPCA_PAIR_CFG", 0);
   const uint32_t kr = (cfg == 1) ? 32 : 16;
   if (!make_x_maps(X, kp2::BM, &tmX, &tmXlo) || !make_x_maps(X, kr, &tmXb, &tmXblo))
     return set_error(c, PPCA_ERR_CUDA, "tensor map X failed");
@@ -820,7 +888,7 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
     c->s_mp = mp;
     c->s_m = m;
   } else {
-    reduce_spart2_kernel<<<(unsigned)ceil_div(m * m, 32), 256, 0, c->stream>>>(Spart, grid, mp, m, S);
+    launch_pdl(reduce_spart2_kernel, dim3((unsigned)ceil_div(m * m, 32)), dim3(256), 0, c->stream, Spart, grid, mp, m, S);
     PPCA_LAUNCH_CHECK(c, "reduce_spart");
   }
   launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
@@ -831,7 +899,7 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
 ppca_status pass_reduce_deferred_s(Ctx* c, double* S, cudaStream_t st) {
   if (!c->s_pending) return PPCA_OK;
   cudaStreamWaitEvent(st, c->s_ev_pass, 0);
-  reduce_spart2_kernel<<<(unsigned)ceil_div(c->s_m * c->s_m, 32), 256, 0, st>>>(c->s_part, c->s_parts, c->s_mp,
+  launch_pdl(reduce_spart2_kernel, dim3((unsigned)ceil_div(c->s_m * c->s_m, 32)), dim3(256), 0, st, c->s_part, c->s_parts, c->s_mp,
                                                                                c->s_m, S);
   PPCA_LAUNCH_CHECK(c, "reduce_spart");
   cudaEventRecord(c->s_ev_red, st);
@@ -885,7 +953,7 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
     const int64_t nb = ceil_div(ldyt, (int64_t)YS_RB);
     double* Sp = (double*)scratch(c, S_NTSTAGE, (size_t)nb * m * m * sizeof(double));
     if (!Sp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-    ysum_s_kernel<<<(unsigned)nb, 256, (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream>>>(Ypart, ksplit, n, mp, m,
+    launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream, Ypart, ksplit, n, mp, m,
                                                                                               YT, ldyt, Sp);
     PPCA_LAUNCH_CHECK(c, "ysum_s");
     PPCA_TRY(launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S));

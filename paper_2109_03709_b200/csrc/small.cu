@@ -19,6 +19,7 @@ constexpr int GRAM_MAXT = 160;                    // threads for m ≤ 128: 136 
 template <int MB>                                 // MB = ceil(m / 8) (≤ 16)
 __global__ void __launch_bounds__(GRAM_MAXT) vec_gram_tiled_kernel(const float* __restrict__ V, int m, int64_t d,
                                                                    int64_t cols_per_split, double* __restrict__ P) {
+  pdl_enter();
   constexpr int MP = MB * 8, LD = MP + 2;         // +2 doubles: 16-byte aligned rows, 4-way worst transposed store
   constexpr int NT = MB * (MB + 1) / 2;           // upper tiles
   constexpr int PER = (MP * GK + GRAM_MAXT - 1) / GRAM_MAXT;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(GRAM_MAXT) vec_gram_tiled_kernel(const float* 
 // G_ij = Σ_x V[i][x] V[j][x]; tile 32×32 outputs × 64-column chunks, split over d.
 __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __restrict__ V, int m, int64_t d,
                                                        int64_t cols_per_split, double* __restrict__ P) {
+  pdl_enter();
   __shared__ float Vi[32][65];
   __shared__ float Vj[32][65];
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __re
 // 2×2 sub-tiles, one per thread (64 + 4 accumulators; the 5-warp kernel above gave one sub-partition two warps).
 __global__ void __launch_bounds__(128) vec_gram_bal16_kernel(const float* __restrict__ V, int m, int64_t d,
                                                              int64_t cols_per_split, double* __restrict__ P) {
+  pdl_enter();
   constexpr int MP = 128, LD = MP + 2, PER = MP * GK / 128;
   __shared__ __align__(16) double sv[GK * LD];
   const int64_t xb = (int64_t)blockIdx.x * cols_per_split;
@@ -258,7 +261,7 @@ size_t vec_gram_part_bytes(const Ctx* c, int m, int64_t d) {
 
 template <int MB>
 static void launch_gram_mb(int nsplit, cudaStream_t st, const float* V, int m, int64_t d, int64_t cps, double* P) {
-  vec_gram_tiled_kernel<MB><<<nsplit, GRAM_MAXT, 0, st>>>(V, m, d, cps, P);
+  launch_pdl(vec_gram_tiled_kernel<MB>, dim3(nsplit), dim3(GRAM_MAXT), 0, st, V, m, d, cps, P);
 }
 
 ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cudaStream_t st, int part_slot) {
@@ -270,7 +273,7 @@ ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cud
   const int mb = (int)ceil_div(m, 8);
   if (gram_short(c, m, d)) {
     const int tiles = (int)ceil_div(m, 32);
-    vec_gram_generic_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, st>>>(V, m, d, cps, P);
+    launch_pdl(vec_gram_generic_kernel, dim3(dim3(tiles, tiles, nsplit)), dim3(256), 0, st, V, m, d, cps, P);
   } else if (mb <= 1) launch_gram_mb<1>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 2) launch_gram_mb<2>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 4) launch_gram_mb<4>(nsplit, st, V, m, d, cps, P);
@@ -278,7 +281,7 @@ ppca_status vec_gram_on(Ctx* c, const float* V, int m, int64_t d, double* G, cud
   else if (mb <= 8) launch_gram_mb<8>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 12) launch_gram_mb<12>(nsplit, st, V, m, d, cps, P);
   else if (mb <= 15) launch_gram_mb<16>(nsplit, st, V, m, d, cps, P);
-  else vec_gram_bal16_kernel<<<nsplit, 128, 0, st>>>(V, m, d, cps, P);
+  else launch_pdl(vec_gram_bal16_kernel, dim3(nsplit), dim3(128), 0, st, V, m, d, cps, P);
   PPCA_LAUNCH_CHECK(c, "vec_gram");
   return launch_reduce_splits_f64(c, P, nsplit, (int64_t)m * m, G, st);
 }
@@ -423,6 +426,7 @@ __device__ unsigned long long g_chol_clk[8];     // phase clocks of the last cho
 
 __global__ void chol_inv_kernel(const double* __restrict__ G, int m, double drop, double* __restrict__ Linv,
                                 int* __restrict__ row_map, int* __restrict__ m_out, int* d_err) {
+  pdl_enter();
   extern __shared__ double sm[];
   if (threadIdx.x == 0) g_chol_clk[0] = clock64();
   const int lda = m | 1;                           // odd row stride: column walks hit distinct banks
@@ -534,6 +538,7 @@ template <int CQ>
 __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
                                                            double* __restrict__ Linv, int* __restrict__ row_map,
                                                            int* __restrict__ m_out, int* d_err) {
+  pdl_enter();
   chol_inv_sweep<CQ>(G, m, Linv, m, nullptr, d_err);
   if (threadIdx.x < m) row_map[threadIdx.x] = threadIdx.x;
   if (threadIdx.x == 0) *m_out = m;
@@ -570,6 +575,7 @@ __device__ __forceinline__ void mm64(const double* __restrict__ A, bool at, cons
 __global__ void __launch_bounds__(512) chol_inv_blk_kernel(const double* __restrict__ G, int m, double* __restrict__ Linv,
                                                            int* __restrict__ row_map, int* __restrict__ m_out,
                                                            int* d_err) {
+  pdl_enter();
   extern __shared__ double cb[];
   double* L11i = cb;                              // L11⁻¹
   double* L21 = L11i + BK64 * BKL;                  // A21, then L21
@@ -613,15 +619,15 @@ static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_m
     static uint64_t attr = 0;
     if (first_on_device(&attr, dev))
       cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    chol_inv_blk_kernel<<<1, 512, smem, st>>>(G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_blk_kernel, dim3(1), dim3(512), smem, st, G, m, Linv, row_map, m_out, d_err);
     return;
   }
   if (g_chol_cq == 4)
-    chol_inv_reg_kernel<4><<<1, 256, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<4>, dim3(1), dim3(256), 0, st, G, m, Linv, row_map, m_out, d_err);
   else if (g_chol_cq == 16)
-    chol_inv_reg_kernel<16><<<1, 1024, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<16>, dim3(1), dim3(1024), 0, st, G, m, Linv, row_map, m_out, d_err);
   else
-    chol_inv_reg_kernel<8><<<1, 512, 0, st>>>(G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<8>, dim3(1), dim3(512), 0, st, G, m, Linv, row_map, m_out, d_err);
 }
 
 static size_t chol_inv_smem(int m) {
@@ -643,6 +649,7 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
                                                          int64_t d, float* __restrict__ OUT, int rows_per_cta) {
+  pdl_enter();
   extern __shared__ double cs[];                 // this CTA's rows × m_in (fp64), then m_in × AP_COLS (fp32)
   const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
   float* ins = reinterpret_cast<float*>(cs + (size_t)rows_per_cta * m_in);
@@ -694,7 +701,7 @@ static ppca_status apply_rows_small(Ctx* c, const double* C, int ldc, int rows, 
   }
   const unsigned gy = (unsigned)ceil_div((int64_t)rows, (int64_t)rpc);
   size_t smem = (size_t)rpc * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
-  apply_rows_kernel<<<dim3((unsigned)gx, gy), 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
+  launch_pdl(apply_rows_kernel, dim3(dim3((unsigned)gx, gy)), dim3(256), smem, st, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
@@ -706,6 +713,7 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
                                                           const int* __restrict__ row_map, bool lower,
                                                           const float* __restrict__ IN, int64_t d,
                                                           float* __restrict__ OUT) {
+  pdl_enter();
   constexpr int RP = 32 * RPT, LDT = RP + 2;      // Cᵀ rows padded: 16-byte aligned, 4-way worst transposed store
   constexpr int PER = (128 * AT_COLS) / 256;      // staged IN values per thread (m_in ≤ 128)
   extern __shared__ __align__(16) double ct[];    // [m_in][LDT] fp64, then [m_in][AT_COLS] fp32
@@ -813,7 +821,7 @@ static void launch_apply_tiled(Ctx* c, const double* C, int ldc, int rows, int m
     cudaFuncSetAttribute(apply_tiled_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int64_t nchunks = ceil_div(d, (int64_t)AT_COLS);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nchunks, c->sm_count));
-  apply_tiled_kernel<RPT><<<grid, 256, smem, st>>>(C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
+  launch_pdl(apply_tiled_kernel<RPT>, dim3(grid), dim3(256), smem, st, C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
 }
 
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
@@ -839,7 +847,7 @@ ppca_status chol_inv_on(Ctx* c, const double* G, int m, double* Linv, int* row_m
     launch_chol_inv_reg(G, m, Linv, row_map, m_out, c->d_err, st);
   } else {
     const size_t smem = chol_inv_smem(m);
-    chol_inv_kernel<<<1, 256, smem, st>>>(G, m, 0.0, Linv, row_map, m_out, c->d_err);
+    launch_pdl(chol_inv_kernel, dim3(1), dim3(256), smem, st, G, m, 0.0, Linv, row_map, m_out, c->d_err);
   }
   PPCA_LAUNCH_CHECK(c, "chol_inv");
   return PPCA_OK;
@@ -875,7 +883,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
     if (m <= 2 * CF_M && g_chol_reg)
       launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
-      chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, 0.0, Linv, row_map, d_mout, c->d_err);
+      launch_pdl(chol_inv_kernel, dim3(1), dim3(256), smem, c->stream, G, m, 0.0, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
     PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, Zin, d, W, c->stream));
     if (m_out) *m_out = m;
@@ -890,7 +898,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
     if (dt <= 0.0 && m <= 2 * CF_M && g_chol_reg)
       launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
-      chol_inv_kernel<<<1, 256, smem, c->stream>>>(G, m, dt, Linv, row_map, d_mout, c->d_err);
+      launch_pdl(chol_inv_kernel, dim3(1), dim3(256), smem, c->stream, G, m, dt, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
     if (pass == 0 && drop_tol > 0.0) {
       int h_m = m;
@@ -1229,6 +1237,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
                                                         float* __restrict__ V, float* __restrict__ vel, int m,
                                                         int64_t d, double alpha, double mu,
                                                         double* __restrict__ rowpart, int* d_err) {
+  pdl_enter();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double egs[];
@@ -1410,9 +1419,19 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
     *st = set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
     return true;
   }
-  void* args[] = {(void*)&MV, (void*)&A, (void*)&V, (void*)&vel, (void*)&m, (void*)&d, (void*)&alpha, (void*)&mu,
-                  (void*)&rowpart, (void*)&c->d_err};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)eg_update_kernel, grid, 256, args, smem, c->stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;                       // one grid barrier: all CTAs co-resident
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // the launch overlaps the Q/P reduction's tail
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, eg_update_kernel, MV, A, V, vel, m, d, alpha, mu, rowpart, c->d_err);
   if (e == cudaErrorCooperativeLaunchTooLarge) {     // not all CTAs co-resident: the 5-launch sequence runs
     cudaGetLastError();
     return false;

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kp2::NTHREADS, 1)
     xwz_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmXlo, const __grid_constant__ CUtensorMap tmXb,
                     KP2Params p) {
+  pdl_wait();   // a programmatic dependent launch: inputs of the previous grid visible
   using namespace kp2;
   constexpr bool LO = XM == 2;
   constexpr uint32_t XSTG = LO ? 2 * XPL : XPL;

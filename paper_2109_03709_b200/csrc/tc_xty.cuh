@@ -49,6 +49,7 @@ template <int MP, bool XBF16, bool XLO = false, bool LEAN = false>
 __global__ void __launch_bounds__(kb::NTHREADS, 1)
     xty_tc_kernel(const __grid_constant__ CUtensorMap tmYT, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, KBParams p) {
+  pdl_wait();   // a programmatic dependent launch: inputs of the previous grid visible
   using namespace kb;
   using CF = Cfg<MP, XLO, LEAN>;
   constexpr int NC = CF::NC, NB = CF::NB, NST = CF::NSTG, NBUF = CF::NBUF;

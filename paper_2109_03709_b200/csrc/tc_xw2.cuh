@@ -68,6 +68,7 @@ template <int MP, int XM, bool PAIR = false>
 __global__ void __launch_bounds__(ka2::NTHREADS, 1)
     xw_tma_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXlo, KAParams p) {
+  pdl_wait();   // a programmatic dependent launch: inputs of the previous grid visible
   using namespace ka2;
   using CF = Cfg<MP, XM, PAIR>;
   static_assert(!PAIR || (MP == 128 && XM == 1), "kernel A2 pairs: MP = 128, bf16 X");
