@@ -701,7 +701,12 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
     plan.precise = true;
     if (X->dtype == PPCA_F32) plan.impl = 1;   // the converter kernels read X_hi only in product 2
     if (plan.impl == 2) {
-      PPCA_TRY(pass_power(c, &Xw, &plan, W, m, Q, P));
+      // one GPU, EigenGame: Z stays as the window pass's row-group partials, summed by the update kernel
+      c->zp_pending = false;
+      c->zp_defer = eigengame && !c->nccl_comm;
+      const ppca_status pst = pass_power(c, &Xw, &plan, W, m, Q, P);
+      c->zp_defer = false;
+      PPCA_TRY(pst);
     } else {
       float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, rows) * m * sizeof(float));
       if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
@@ -711,10 +716,13 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
       PPCA_TRY(yty(c, Y, m, rows, P));
     }
     PPCA_TRY(allreduce_zs(c, Q, (size_t)m * d, P, (size_t)m * m));
-    if (eigengame)
+    if (eigengame) {
       PPCA_TRY(eigengame_update(c, Q, P, W, vel, m, d, alpha, mu));
-    else
+    } else {
+      PPCA_TRY(pass_reduce_deferred_z(c, Q));
       PPCA_TRY(oja_update(c, Q, P, W, vel, m, d, alpha, mu));
+    }
+    c->zp_pending = false;
   }
   *step_io = s0 + steps;
   return PPCA_OK;

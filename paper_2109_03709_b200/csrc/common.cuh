@@ -44,6 +44,12 @@ struct Ctx {
   cudaEvent_t s_ev_pass = nullptr, s_ev_red = nullptr;
   const double* s_part = nullptr;
   int s_parts = 0, s_mp = 0, s_m = 0;
+  // deferred Z reduction (EigenGame steps on one GPU): the window pass leaves its row-group partials and the
+  // update kernel sums them while staging (pass_reduce_deferred_z reduces them for any other consumer)
+  bool zp_defer = false, zp_pending = false;
+  const float* zp_part = nullptr;
+  int64_t zp_nrg = 0, zp_dpad = 0, zp_d = 0;
+  int zp_mp = 0, zp_m = 0;
   bool side_busy = false;             // side-stream kernels may overlap the next pass: persistent
                                       // pass kernels then leave one SM free (a late CTA stalls the pass)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -107,6 +113,7 @@ ppca_status check_cuda(Ctx* c, cudaError_t e, const char* what);
 ppca_status finish(Ctx* c, const char* what);      // sync stream, read error word, map to status
 ppca_status allreduce(Ctx* c, void* buf, size_t count, bool f64);
 ppca_status allreduce_zs(Ctx* c, float* Z, size_t nz, double* S, size_t ns);   // grouped [Z | S]
+ppca_status pass_reduce_deferred_z(Ctx* c, float* Z);   // Z from the partials a deferred pass left (no-op otherwise)
 
 #define PPCA_TRY(expr)                         \
   do {                                         \

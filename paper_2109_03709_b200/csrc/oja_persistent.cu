@@ -481,7 +481,8 @@ bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oja_persistent_kernel, OJA_THREADS, OJA_SMEM);
   if (per_sm < 1) return false;
-  const int grid = c->sm_count;
+  static const int grid_env = tune_env("PPCA_OJA_GRID", 0);   // experiment builds: fewer CTAs
+  const int grid = grid_env > 0 ? std::min(grid_env, c->sm_count) : c->sm_count;
   OjaParams p;
   p.X = X->data; p.xdtype = (int)X->dtype; p.ld = X->ld; p.n = X->n_local; p.d = d;
   p.m = m; p.batch = batch; p.s0 = s0; p.steps = steps;

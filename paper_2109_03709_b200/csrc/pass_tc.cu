@@ -1001,7 +1001,25 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
   else
     PPCA_TRY((dispatch_kb<true, false>(c, mp, tmYT, tmX, tmXlo, bp, grid)));
   kernel_timer_mark(c, 1);
+  if (c->zp_defer && bp.nrg <= 16 && c->z_block_cols == 0) {   // the EigenGame update sums the partials itself
+    c->zp_pending = true;
+    c->zp_part = Zp;
+    c->zp_nrg = bp.nrg;
+    c->zp_dpad = dpad;
+    c->zp_mp = mp;
+    c->zp_m = m;
+    c->zp_d = d;
+    return PPCA_OK;
+  }
   launch_reduce_zp(c, Zp, bp.nrg, dpad, mp, m, d, Z);
+  PPCA_LAUNCH_CHECK(c, "reduce_zp");
+  return PPCA_OK;
+}
+
+ppca_status pass_reduce_deferred_z(Ctx* c, float* Z) {
+  if (!c->zp_pending) return PPCA_OK;
+  c->zp_pending = false;
+  launch_reduce_zp(c, c->zp_part, c->zp_nrg, c->zp_dpad, c->zp_mp, c->zp_m, c->zp_d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");
   return PPCA_OK;
 }

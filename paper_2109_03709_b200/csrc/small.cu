@@ -1233,10 +1233,59 @@ __global__ void eg_elementwise_kernel(const float* __restrict__ MV, const float*
 // barrier; then every CTA sums the chunks' row partials in chunk order (identical in all CTAs) and rescales
 // its columns.  Same arithmetic as eg_coeff + apply_rows + eg_elementwise + normalize_rows.
 constexpr int EG_XC = 32;
+constexpr int EG_ZPMAX = 16;    // row-group partials of Z summed while staging (the window pass's nrg ≤ 16)
+// MV of this chunk into mvs[j][xl]: from the reduced MV, or (Zp != null) straight from the tensor-core window
+// pass's row-group partials Zp[g][x][mp] — summed in g order in fp64 and rounded to fp32 exactly as the
+// reduction kernel (reduce_zp) would have stored Z, so the result is bitwise the same without that launch
+__device__ __forceinline__ void eg_stage_mv(const float* __restrict__ MV, const float* __restrict__ Zp, int64_t nrg,
+                                            int64_t dpad, int mp, int m, int64_t d, int64_t x0, float* mvs) {
+  const int tid = threadIdx.x;
+  if (!Zp) {
+    copy_batched<8>(tid, (int64_t)m * EG_XC, blockDim.x,
+                    [&](int64_t e) {
+                      const int64_t x = x0 + e % EG_XC;
+                      return MV[(e / EG_XC) * d + (x < d ? x : d - 1)];
+                    },
+                    [&](int64_t e, float v) { mvs[e] = v; });
+    return;
+  }
+  const int q4 = mp >> 2;
+  for (int it = tid; it < EG_XC * q4; it += blockDim.x) {
+    const int xl = it / q4, j4 = (it % q4) * 4;
+    const int64_t x = min(x0 + xl, d - 1);
+    const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
+    const int64_t gs = dpad * mp / 4;
+    float4 v[EG_ZPMAX];
+#pragma unroll
+    for (int g = 0; g < EG_ZPMAX; ++g)
+      if (g < nrg) v[g] = __ldg(src + g * gs);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int g = 0; g < EG_ZPMAX; ++g)
+      if (g < nrg) {
+        a0 += (double)v[g].x; a1 += (double)v[g].y; a2 += (double)v[g].z; a3 += (double)v[g].w;
+      }
+    if (j4 < m) mvs[j4 * EG_XC + xl] = (float)a0;
+    if (j4 + 1 < m) mvs[(j4 + 1) * EG_XC + xl] = (float)a1;
+    if (j4 + 2 < m) mvs[(j4 + 2) * EG_XC + xl] = (float)a2;
+    if (j4 + 3 < m) mvs[(j4 + 3) * EG_XC + xl] = (float)a3;
+  }
+}
+
+// The whole EigenGame update in ONE cooperative kernel (the 5-launch sequence above costs ≈ 37 µs per C4 step,
+// latency-bound): every CTA forms Cf = A_ji/A_ii and 2U from A itself (m×m, in shared memory — no barrier needed), then
+// per 32-column chunk (lane = column, warp = rows j ≡ w mod 8): T_j = Σ_{i<j} Cf_ji·MV_i from a staged MV slab,
+// r, Nesterov, V (unnormalised, rounded to fp32 as stored) and this chunk's Σ_x V_jx² per row; one grid
+// barrier; then every CTA sums the chunks' row partials in chunk order (identical in all CTAs) and rescales
+// its columns.  Same arithmetic as eg_coeff + apply_rows + eg_elementwise + normalize_rows.
+// Latency: the first chunk's V, velocity and MV loads are issued before the m×m coefficient work (one round
+// trip for all of them), and the row partials after the barrier are summed with every load in flight.
 __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict__ MV, const double* __restrict__ A,
                                                         float* __restrict__ V, float* __restrict__ vel, int m,
                                                         int64_t d, double alpha, double mu,
-                                                        double* __restrict__ rowpart, int* d_err) {
+                                                        double* __restrict__ rowpart, int* d_err,
+                                                        const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
+                                                        int mp) {
   pdl_enter();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1249,6 +1298,19 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
   __shared__ double amax;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t nchunks = (d + EG_XC - 1) / EG_XC;
+  // this warp's V and velocity entries of the chunk (≤ PPCA_MAX_M / 8 rows per warp), in flight early
+  float vpre[PPCA_MAX_M / 8], velpre[PPCA_MAX_M / 8];
+  auto prefetch_vv = [&](int64_t ch) {
+    const int64_t x = ch * EG_XC + lane;
+#pragma unroll
+    for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+      const int j = warp + q * nw;
+      const bool ok = j < m && x < d && ch < nchunks;
+      vpre[q] = ok ? V[(int64_t)j * d + x] : 0.f;
+      velpre[q] = ok ? vel[(int64_t)j * d + x] : 0.f;
+    }
+  };
+  prefetch_vv(blockIdx.x);
   // coefficients (eg_coeff_kernel's arithmetic)
   if (warp == 0) {
     double mx = 0.0;
@@ -1258,6 +1320,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
   }
   copy_batched<16>(tid, (int64_t)m * m, blockDim.x, [&](int64_t e) { return A[e]; },
                    [&](int64_t e, double v) { Cf[e] = v; });
+  if (blockIdx.x < nchunks) eg_stage_mv(MV, Zp, nrg, dpad, mp, m, d, (int64_t)blockIdx.x * EG_XC, mvs);
   __syncthreads();
   for (int i = tid; i < m; i += blockDim.x) {
     double aii = Cf[i * m + i];
@@ -1300,23 +1363,12 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
   for (int q = 0; q < PPCA_MAX_M / 8; ++q) racc[q] = 0.0;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t x0 = ch * EG_XC;
-    copy_batched<8>(tid, (int64_t)m * EG_XC, blockDim.x,
-                    [&](int64_t e) {
-                      const int64_t x = x0 + e % EG_XC;
-                      return MV[(e / EG_XC) * d + (x < d ? x : d - 1)];
-                    },
-                    [&](int64_t e, float v) { mvs[e] = v; });
-    __syncthreads();
-    const int64_t x = x0 + lane;
-    // this warp's V and velocity entries, all in flight before the row loop (≤ PPCA_MAX_M / 8 rows per warp)
-    float vpre[PPCA_MAX_M / 8], velpre[PPCA_MAX_M / 8];
-#pragma unroll
-    for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
-      const int j = warp + q * nw;
-      const bool ok = j < m && x < d;
-      vpre[q] = ok ? V[(int64_t)j * d + x] : 0.f;
-      velpre[q] = ok ? vel[(int64_t)j * d + x] : 0.f;
+    if (ch != blockIdx.x) {                            // later chunks (grid < chunks): staged here
+      eg_stage_mv(MV, Zp, nrg, dpad, mp, m, d, x0, mvs);
+      prefetch_vv(ch);
+      __syncthreads();
     }
+    const int64_t x = x0 + lane;
 #pragma unroll
     for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
       const int j = warp + q * nw;
@@ -1361,14 +1413,14 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
     }
   }
   grid.sync();
-  // row norms: thread (row j, slice s) sums the CTA partials c ≡ s (mod ns) in order (8 loads in flight), the slices
-  // are added in slice order — the same sums in every CTA; then this CTA's columns are rescaled
+  // row norms: thread (row j, slice s) sums the CTA partials c ≡ s (mod ns) in order (all loads in flight), the
+  // slices are added in slice order — the same sums in every CTA; then this CTA's columns are rescaled
   {
     const int ns = (int)blockDim.x / m;                   // ≥ 2 for m ≤ 128
     const int j = threadIdx.x % m, sl = threadIdx.x / m;
     double* part = reinterpret_cast<double*>(mvs);        // ns × m (the MV slab is free now)
     if (sl < ns)
-      part[sl * m + j] = sum_in_order<8>(sl, (int64_t)gridDim.x, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
+      part[sl * m + j] = sum_in_order<32>(sl, (int64_t)gridDim.x, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
     __syncthreads();
     if (threadIdx.x < m) {
       double s2 = 0.0;
@@ -1431,7 +1483,19 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, eg_update_kernel, MV, A, V, vel, m, d, alpha, mu, rowpart, c->d_err);
+  // Z straight from the window pass's row-group partials when it left them (pass_defer_z)
+  const float* Zp = nullptr;
+  int64_t nrg = 0, dpad = 0;
+  int mp = 0;
+  if (c->zp_pending) {
+    Zp = c->zp_part;
+    nrg = c->zp_nrg;
+    dpad = c->zp_dpad;
+    mp = c->zp_mp;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, eg_update_kernel, MV, A, V, vel, m, d, alpha, mu, rowpart, c->d_err, Zp,
+                                     nrg, dpad, mp);
+  if (e == cudaSuccess) c->zp_pending = false;
   if (e == cudaErrorCooperativeLaunchTooLarge) {     // not all CTAs co-resident: the 5-launch sequence runs
     cudaGetLastError();
     return false;
@@ -1449,6 +1513,7 @@ ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V,
     ppca_status st;
     if (eigengame_update_fused(c, MV, A, V, vel, m, d, alpha, mu, &st)) return st;
   }
+  PPCA_TRY(pass_reduce_deferred_z(c, const_cast<float*>(MV)));   // the multi-launch sequence reads Z itself
   double* Cf = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + (size_t)m * sizeof(double) + 64);
   double* twoU = Cf + (size_t)m * m;
   float* T = (float*)scratch(c, S_W3, (size_t)m * d * sizeof(float));
