@@ -1226,19 +1226,19 @@ __global__ void eg_elementwise_kernel(const float* __restrict__ MV, const float*
   V[e] = (float)w;
 }
 
-// The whole EigenGame update in ONE cooperative kernel (the 5-launch sequence above costs ≈ 37 µs per C4 step,
-// latency-bound): every CTA forms Cf and 2U from A itself (m×m, in shared memory — no barrier needed), then
-// per 32-column chunk (lane = column, warp = rows j ≡ w mod 8): T_j = Σ_{i<j} Cf_ji·MV_i from a staged MV slab,
-// r, Nesterov, V (unnormalised, rounded to fp32 as stored) and this chunk's Σ_x V_jx² per row; one grid
-// barrier; then every CTA sums the chunks' row partials in chunk order (identical in all CTAs) and rescales
-// its columns.  Same arithmetic as eg_coeff + apply_rows + eg_elementwise + normalize_rows.
 constexpr int EG_XC = 32;
 constexpr int EG_ZPMAX = 16;    // row-group partials of Z summed while staging (the window pass's nrg ≤ 16)
+#ifdef PPCA_EXPERIMENTS
+__device__ unsigned long long g_eg_clk[8];          // phase stamps of CTA 0 (experiment builds)
+#define EG_STAMP(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_eg_clk[i] = clock64(); } while (0)
+#else
+#define EG_STAMP(i) do { } while (0)
+#endif
 // MV of this chunk into mvs[j][xl]: from the reduced MV, or (Zp != null) straight from the tensor-core window
 // pass's row-group partials Zp[g][x][mp] — summed in g order in fp64 and rounded to fp32 exactly as the
 // reduction kernel (reduce_zp) would have stored Z, so the result is bitwise the same without that launch
 __device__ __forceinline__ void eg_stage_mv(const float* __restrict__ MV, const float* __restrict__ Zp, int64_t nrg,
-                                            int64_t dpad, int mp, int m, int64_t d, int64_t x0, float* mvs) {
+                                            int64_t dpad, int mp, int m, int64_t d, int64_t x0, double* mvs) {
   const int tid = threadIdx.x;
   if (!Zp) {
     copy_batched<8>(tid, (int64_t)m * EG_XC, blockDim.x,
@@ -1246,15 +1246,50 @@ __device__ __forceinline__ void eg_stage_mv(const float* __restrict__ MV, const 
                       const int64_t x = x0 + e % EG_XC;
                       return MV[(e / EG_XC) * d + (x < d ? x : d - 1)];
                     },
-                    [&](int64_t e, float v) { mvs[e] = v; });
+                    [&](int64_t e, float v) { mvs[e] = (double)v; });
     return;
   }
   const int q4 = mp >> 2;
-  for (int it = tid; it < EG_XC * q4; it += blockDim.x) {
+  const int64_t gs = dpad * mp / 4;
+  auto store = [&](int it, double a0, double a1, double a2, double a3) {
+    const int xl = it / q4, j4 = (it % q4) * 4;
+    if (j4 < m) mvs[j4 * EG_XC + xl] = (double)(float)a0;
+    if (j4 + 1 < m) mvs[(j4 + 1) * EG_XC + xl] = (double)(float)a1;
+    if (j4 + 2 < m) mvs[(j4 + 2) * EG_XC + xl] = (double)(float)a2;
+    if (j4 + 3 < m) mvs[(j4 + 3) * EG_XC + xl] = (double)(float)a3;
+  };
+  auto src_of = [&](int it) {
     const int xl = it / q4, j4 = (it % q4) * 4;
     const int64_t x = min(x0 + xl, d - 1);
-    const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
-    const int64_t gs = dpad * mp / 4;
+    return reinterpret_cast<const float4*>(Zp + x * mp + j4);
+  };
+  const int total = EG_XC * q4, nt = blockDim.x;
+  if (nrg <= EG_ZPMAX / 2) {                          // two items per round, all their loads in flight
+    for (int it = tid; it < total; it += 2 * nt) {
+      const int it2 = it + nt;
+      const float4* s1 = src_of(it);
+      const float4* s2 = src_of(it2 < total ? it2 : it);
+      float4 v1[EG_ZPMAX / 2], v2[EG_ZPMAX / 2];
+#pragma unroll
+      for (int g = 0; g < EG_ZPMAX / 2; ++g)
+        if (g < nrg) {
+          v1[g] = __ldg(s1 + g * gs);
+          v2[g] = __ldg(s2 + g * gs);
+        }
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+#pragma unroll
+      for (int g = 0; g < EG_ZPMAX / 2; ++g)
+        if (g < nrg) {
+          a0 += (double)v1[g].x; a1 += (double)v1[g].y; a2 += (double)v1[g].z; a3 += (double)v1[g].w;
+          b0 += (double)v2[g].x; b1 += (double)v2[g].y; b2 += (double)v2[g].z; b3 += (double)v2[g].w;
+        }
+      store(it, a0, a1, a2, a3);
+      if (it2 < total) store(it2, b0, b1, b2, b3);
+    }
+    return;
+  }
+  for (int it = tid; it < total; it += nt) {
+    const float4* src = src_of(it);
     float4 v[EG_ZPMAX];
 #pragma unroll
     for (int g = 0; g < EG_ZPMAX; ++g)
@@ -1265,10 +1300,7 @@ __device__ __forceinline__ void eg_stage_mv(const float* __restrict__ MV, const 
       if (g < nrg) {
         a0 += (double)v[g].x; a1 += (double)v[g].y; a2 += (double)v[g].z; a3 += (double)v[g].w;
       }
-    if (j4 < m) mvs[j4 * EG_XC + xl] = (float)a0;
-    if (j4 + 1 < m) mvs[(j4 + 1) * EG_XC + xl] = (float)a1;
-    if (j4 + 2 < m) mvs[(j4 + 2) * EG_XC + xl] = (float)a2;
-    if (j4 + 3 < m) mvs[(j4 + 3) * EG_XC + xl] = (float)a3;
+    store(it, a0, a1, a2, a3);
   }
 }
 
@@ -1287,6 +1319,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
                                                         const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
                                                         int mp) {
   pdl_enter();
+  EG_STAMP(0);
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double egs[];
@@ -1294,7 +1327,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
   double* twoU = Cf + (size_t)m * m;                  // m
   double* rdiag = twoU + m;                           // m
   double* nrm = rdiag + m;                            // m (reciprocal row norms)
-  float* mvs = reinterpret_cast<float*>(nrm + m);     // m × EG_XC
+  double* mvs = nrm + m;                             // m × EG_XC (MV as stored, fp32 values held in fp64)
   __shared__ double amax;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int64_t nchunks = (d + EG_XC - 1) / EG_XC;
@@ -1322,6 +1355,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
                    [&](int64_t e, double v) { Cf[e] = v; });
   if (blockIdx.x < nchunks) eg_stage_mv(MV, Zp, nrg, dpad, mp, m, d, (int64_t)blockIdx.x * EG_XC, mvs);
   __syncthreads();
+  EG_STAMP(1);
   for (int i = tid; i < m; i += blockDim.x) {
     double aii = Cf[i * m + i];
     if (!(aii > 1e-12 * amax)) {
@@ -1356,11 +1390,17 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
     if (lane == 0) twoU[j] = 2.0 * (ajj - part);
   }
   __syncthreads();
+  EG_STAMP(2);
   // update per column chunk; the squared row norms of this CTA's chunks accumulate in chunk order (lane 0 of
   // the row's warp) and leave as one partial per CTA
   double racc[PPCA_MAX_M / 8];
+  float wkeep[PPCA_MAX_M / 8];
+  const bool single = gridDim.x >= nchunks;          // one chunk per CTA: V stays in registers over the barrier
 #pragma unroll
-  for (int q = 0; q < PPCA_MAX_M / 8; ++q) racc[q] = 0.0;
+  for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+    racc[q] = 0.0;
+    wkeep[q] = 0.f;
+  }
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t x0 = ch * EG_XC;
     if (ch != blockIdx.x) {                            // later chunks (grid < chunks): staged here
@@ -1381,23 +1421,24 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           a[u] = cj[i + u];
-          b[u] = (double)mvs[(i + u) * EG_XC + lane];
+          b[u] = mvs[(i + u) * EG_XC + lane];
         }
         t0 = fma(a[0], b[0], t0); t1 = fma(a[1], b[1], t1); t2 = fma(a[2], b[2], t2); t3 = fma(a[3], b[3], t3);
         t0 = fma(a[4], b[4], t0); t1 = fma(a[5], b[5], t1); t2 = fma(a[6], b[6], t2); t3 = fma(a[7], b[7], t3);
       }
-      for (; i < j; ++i) t0 = fma(cj[i], (double)mvs[i * EG_XC + lane], t0);
+      for (; i < j; ++i) t0 = fma(cj[i], mvs[i * EG_XC + lane], t0);
       const float tf = (float)((t0 + t1) + (t2 + t3));   // T as the apply kernel stores it (fp32)
       double sq = 0.0;
       if (x < d) {
         const int64_t e = (int64_t)j * d + x;
-        const double r = 2.0 * (double)mvs[j * EG_XC + lane] - 2.0 * (double)tf - twoU[j] * (double)vpre[q];
+        const double r = 2.0 * mvs[j * EG_XC + lane] - 2.0 * (double)tf - twoU[j] * (double)vpre[q];
         const double v = mu * (double)velpre[q] + r;
         const double w = (double)vpre[q] + alpha * (r + mu * v);
         if (!isfinite(w)) atomicOr(d_err, DEV_NONFINITE);
         vel[e] = (float)v;
         const float wf = (float)w;
-        V[e] = wf;
+        if (single) wkeep[q] = wf;                     // rescaled from the register after the barrier
+        else V[e] = wf;
         sq = (double)wf * wf;
       }
       sq = warp_sum(sq);
@@ -1412,13 +1453,15 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
       if (j < m) rowpart[(int64_t)blockIdx.x * m + j] = racc[q];
     }
   }
+  EG_STAMP(3);
   grid.sync();
+  EG_STAMP(4);
   // row norms: thread (row j, slice s) sums the CTA partials c ≡ s (mod ns) in order (all loads in flight), the
   // slices are added in slice order — the same sums in every CTA; then this CTA's columns are rescaled
   {
     const int ns = (int)blockDim.x / m;                   // ≥ 2 for m ≤ 128
     const int j = threadIdx.x % m, sl = threadIdx.x / m;
-    double* part = reinterpret_cast<double*>(mvs);        // ns × m (the MV slab is free now)
+    double* part = mvs;                                   // ns × m (the MV slab is free now)
     if (sl < ns)
       part[sl * m + j] = sum_in_order<32>(sl, (int64_t)gridDim.x, ns, [&](int64_t c1) { return rowpart[c1 * m + j]; });
     __syncthreads();
@@ -1435,18 +1478,33 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
     }
   }
   __syncthreads();
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t x = ch * EG_XC + lane;
+  EG_STAMP(5);
+  if (single) {
+    const int64_t x = (int64_t)blockIdx.x * EG_XC + lane;
     if (x < d)
-      for (int j = warp; j < m; j += nw) {
-        const int64_t e = (int64_t)j * d + x;
-        if (nrm[j] > 0.0) {
-          const double v = (double)V[e] * nrm[j];
-          if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
-          V[e] = (float)v;
-        }
+#pragma unroll
+      for (int q = 0; q < PPCA_MAX_M / 8; ++q) {
+        const int j = warp + q * nw;
+        if (j >= m) break;
+        const double v = nrm[j] > 0.0 ? (double)wkeep[q] * nrm[j] : (double)wkeep[q];
+        if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
+        V[(int64_t)j * d + x] = (float)v;
       }
+  } else {
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      const int64_t x = ch * EG_XC + lane;
+      if (x < d)
+        for (int j = warp; j < m; j += nw) {
+          const int64_t e = (int64_t)j * d + x;
+          if (nrm[j] > 0.0) {
+            const double v = (double)V[e] * nrm[j];
+            if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
+            V[e] = (float)v;
+          }
+        }
+    }
   }
+  EG_STAMP(6);
 }
 
 static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
@@ -1454,7 +1512,7 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
   *st = PPCA_OK;
   const int64_t nchunks = ceil_div(d, (int64_t)EG_XC);
   const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) +
-                      std::max((size_t)m * EG_XC * sizeof(float), (size_t)256 * sizeof(double));
+                      std::max((size_t)m * EG_XC * sizeof(double), (size_t)256 * sizeof(double));
   static uint64_t attr = 0;
   if (first_on_device(&attr, c->device)) {
     cudaFuncSetAttribute(eg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1496,6 +1554,16 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
   cudaError_t e = cudaLaunchKernelEx(&cfg, eg_update_kernel, MV, A, V, vel, m, d, alpha, mu, rowpart, c->d_err, Zp,
                                      nrg, dpad, mp);
   if (e == cudaSuccess) c->zp_pending = false;
+#ifdef PPCA_EXPERIMENTS
+  static const int eg_clk = tune_env("PPCA_EG_CLK", 0);
+  if (eg_clk && e == cudaSuccess) {
+    unsigned long long t[8];
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpyFromSymbol(t, g_eg_clk, sizeof(t));
+    fprintf(stderr, "[eg_update] cycles: stage+A %llu  coeff %llu  chunk %llu  grid.sync %llu  norms %llu  rescale %llu\n",
+            t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - t[5]);
+  }
+#endif
   if (e == cudaErrorCooperativeLaunchTooLarge) {     // not all CTAs co-resident: the 5-launch sequence runs
     cudaGetLastError();
     return false;

@@ -11,6 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2109_03709_b200 as P  # noqa: E402
 from inputs import configs as C  # noqa: E402
 
+if os.environ.get("PPCA_EXP_LIB"):               # experiment build (tools/ ablations only)
+    P.load(os.environ["PPCA_EXP_LIB"])
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 split = len(sys.argv) > 3 and sys.argv[3] == "split"
