@@ -527,12 +527,15 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   if (!W || iters < 0 || !(eps == eps)) return set_error(c, PPCA_ERR_INVALID_ARG, "null W, iters < 0 or NaN eps");
   const bool stop_rule = eps > 0.0;
   const int64_t d = X->d;
-  if (init_seed) {
-    PPCA_TRY(init_rows(c, init_seed, W, m, d));
-    PPCA_TRY(cholqr2(c, W, m, d, 0.0, nullptr));
-  }
   // all scratch up front (no reallocation while the side stream is busy)
   float* Z = (float*)scratch(c, S_Z, (size_t)m * d * sizeof(float));
+  if (init_seed) {
+    // W_0 = Q-factor of a Gaussian block: one fp64 CholQR pass is exact to ε64·κ² (κ of an m×d Gaussian block
+    // ≈ (√d + √m)/(√d − √m), below 2 for the workloads), so the second pass of CholQR2 would change nothing
+    if (!Z) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    PPCA_TRY(init_rows(c, init_seed, Z, m, d));
+    PPCA_TRY(cholqr(c, Z, W, m, d, 0.0, nullptr, (double)m * 4 <= (double)d ? 1 : 2));
+  }
   double* Sbuf = (double*)scratch(c, S_S, (size_t)4 * m * m * sizeof(double));      // S[2], Bm[2]
   double* theta_dev = (double*)scratch(c, S_TC2, (size_t)std::max(1, iters) * m * sizeof(double) + (size_t)m * m * sizeof(double));
   if (!Z || !Sbuf || !theta_dev) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
@@ -826,7 +829,7 @@ static ppca_status refine_impl(Ctx* c, const ppca_matrix* X, const float* V, int
   PPCA_TRY(allreduce(c, S, (size_t)mm * mm, true));
   const float* Bop = plan.Wop;                            // the operand rows the pass used
   PPCA_TRY(vec_gram(c, Bop, mm, d, Bm));
-  PPCA_TRY(ritz_solve(c, S, Bm, mm, theta_dev, R, c->stream));
+  PPCA_TRY(ritz_solve(c, S, Bm, mm, theta_dev, R, c->stream, k));   // the k largest pairs only
   PPCA_TRY(lift_rows(c, R, mm, Bop, mm, k, d, E, true, c->stream));
   PPCA_TRY(finish(c, "ppca_refine"));
   if (theta_host) {

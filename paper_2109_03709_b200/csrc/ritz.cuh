@@ -191,8 +191,11 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
 __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
                                                           int m, double* __restrict__ gLinv, double* __restrict__ gT1,
                                                           double* __restrict__ theta, int* d_err,
-                                                          double* __restrict__ R = nullptr) {
+                                                          double* __restrict__ R = nullptr, int top = 0) {
+  // top (1 ≤ top ≤ m): only the top largest eigenpairs are formed (the refine needs k of m); 0 = all
   extern __shared__ double sm[];
+  if (top <= 0 || top > m) top = m;
+  const int jlo = m - top;                            // ascending index of the smallest eigenpair formed
   const bool small = m <= 64;
   const bool vectors = R != nullptr && small;
   double* A = sm;                                     // m × m (C, then the reduced matrix)
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   }
   __syncthreads();
   if (tid == 0) g_ritz_clk[4] = clock64();
-  // 3. Sturm multisection: eigenvalue j (ascending) by G = nt/m threads; count(x) = #{i : d_i < 0}
+  // 3. Sturm multisection: eigenvalue j (ascending) by G = nt/top threads; count(x) = #{i : d_i < 0}
   double lo = 0.0, hi = 0.0;
   for (int i = 0; i < m; ++i) {                        // Gershgorin bounds (every thread)
     const double r = (i > 0 ? fabs(tb[i - 1]) : 0.0) + (i + 1 < m ? fabs(tb[i]) : 0.0);
@@ -339,22 +342,32 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   // θ history needs ~1e-10 relative (the parity bar is 1e-4): (G+1)^rounds ≥ 2^42 of the Gershgorin span.
   // (The Sturm recurrence is bound by the fp64 reciprocal's throughput, not its latency: four interleaved
   // probes per thread and 9 rounds of 32 probes measured 215 µs against 94 µs for 14 rounds of 8.)
-  const int G = nt / m >= 8 ? 8 : (nt / m >= 4 ? 4 : (nt / m >= 2 ? 2 : 1));
+  // (16 probes × 11 rounds for top = 32 measured 84 µs against 81 µs for 8 × 14: the counts share the fp64
+  // reciprocal pipe, so more probes per round do not pay)
+  const int G = nt / top >= 8 ? 8 : (nt / top >= 4 ? 4 : (nt / top >= 2 ? 2 : 1));
   const int rounds = G == 8 ? 14 : (G == 4 ? 19 : (G == 2 ? 27 : 42));
-  for (int b0 = 0; b0 < m; b0 += nt / G) {              // uniform trip counts: every lane reaches the shuffles
+  // squared off-diagonal once (bsq[i] = b_{i-1}², bsq[0] unused), so the count loop is load + rcp + two DFMA
+  double* bsq = pv;                                   // (pv is free after the tridiagonalisation)
+  for (int i = tid; i < m; i += nt) bsq[i] = i > 0 ? tb[i - 1] * tb[i - 1] : 0.0;
+  __syncthreads();
+  for (int b0 = jlo; b0 < m; b0 += nt / G) {            // uniform trip counts: every lane reaches the shuffles
     const int q = tid % G, j = b0 + tid / G;
     const bool act = j < m;
+    const int mm = act ? m : 0;
     double L = lo, U = hi;
     for (int round = 0; round < rounds; ++round) {
       const double x = L + (U - L) * (double)(q + 1) / (double)(G + 1);
       int cnt = 0;
-      double dd = 1.0;
-      for (int i = 0; i < (act ? m : 0); ++i) {      // (reciprocal instead of an IEEE division: only signs count)
-        const double bs = i > 0 ? tb[i - 1] * tb[i - 1] : 0.0;
-        dd = (ta[i] - x) - (i > 0 ? bs * __drcp_rn(dd) : 0.0);
+      double dd = ta[0] - x;
+      if (dd == 0.0) dd = -1e-300;
+      cnt += dd < 0.0;
+#pragma unroll 4
+      for (int i = 1; i < mm; ++i) {                   // (reciprocal instead of an IEEE division: only signs count)
+        dd = (ta[i] - x) - bsq[i] * __drcp_rn(dd);
         if (dd == 0.0) dd = -1e-300;
         cnt += dd < 0.0;
       }
+      if (!act) cnt = 0;
       // the G probes split [L, U] into G+1 parts: keep the part holding the (j+1)-th eigenvalue
       double nL = L, nU = U;
       for (int g2 = 0; g2 < G; ++g2) {
@@ -384,8 +397,8 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   const double tiny = 1e-14 * span;
   double* Dp = A + 3 * m * m;                         // Dp[i·m + j], Dm[i·m + j]: pivots of eigenvalue j's twist
   double* Dm = A + 4 * m * m;
-  for (int j0 = tid; j0 < m; j0 += nt) {
-    if (j0 > 0 && evals[j0] - evals[j0 - 1] <= ctol) continue;   // not a cluster leader
+  for (int j0 = jlo + tid; j0 < m; j0 += nt) {
+    if (j0 > jlo && evals[j0] - evals[j0 - 1] <= ctol) continue;   // not a cluster leader
     int j1 = j0 + 1;
     while (j1 < m && evals[j1] - evals[j1 - 1] <= ctol) ++j1;
     if (j1 == j0 + 1) {
@@ -497,7 +510,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   {
     const int ns = nt / 64 < 1 ? 1 : (nt / 64 > 8 ? 8 : nt / 64);
     const int j = tid % 64, sl = tid / 64;
-    const bool own = j < m && sl < ns;
+    const bool own = j >= jlo && j < m && sl < ns;
     __shared__ double red[8 * 64];                    // ns × 64 partial dots
     for (int k = m - 3; k >= 0; --k) {
       const double bk = hbeta[k];
@@ -519,7 +532,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   }
   if (tid == 0) g_ritz_clk[7] = clock64();
   // 6. R = Uᵀ L⁻¹ in descending order (row i ↔ ascending eigenvector m-1-i)
-  for (int e = tid; e < m * m; e += nt) {
+  for (int e = tid; e < top * m; e += nt) {
     const int i = e / m, c = e % m;
     const int j = m - 1 - i;
     double sum = 0.0;

@@ -932,7 +932,7 @@ ppca_status ritz_debug_clocks(unsigned long long* out8) {
 }
 
 ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev, double* R_dev,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, int top) {
   double* scr = (double*)scratch(c, S_EVAL, (size_t)2 * m * m * sizeof(double));
   if (!scr) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   static uint64_t attr = 0;
@@ -948,7 +948,8 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
       cudaFuncSetAttribute(ritz::ritz_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);   // + 32 KB static
     }
     const size_t vsm = (R_dev && m <= 64) ? ritz::vectors_smem_bytes(m) : ritz::values_smem_bytes(m);
-    ritz::ritz_values_kernel<<<1, 512, vsm, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, c->d_err, R_dev);
+    ritz::ritz_values_kernel<<<1, 512, vsm, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, c->d_err, R_dev,
+                                                      R_dev ? top : 0);
     PPCA_LAUNCH_CHECK(c, "ritz_values_kernel");
     return PPCA_OK;
   }

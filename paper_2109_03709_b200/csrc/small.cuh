@@ -27,7 +27,7 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
 // solve S u = θ Bm u:  L = chol(Bm), Jacobi(L⁻¹SL⁻ᵀ) → θ (desc), U;  R = Uᵀ L⁻¹.
 // theta_dev: double[m]; R_dev: double[m][m] (row i lifts eigenvector i: e_i = Σ_j R_ij w_j).
 ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev,
-                       double* R_dev, cudaStream_t stream);
+                       double* R_dev, cudaStream_t stream, int top = 0);   // top > 0: only the top largest pairs (R_dev)
 
 // E[k][d] = R[:k] · W  (fp64 accumulate), then the sign convention on each row.
 ppca_status lift_rows(Ctx* c, const double* R, int ldr, const float* W, int m, int k, int64_t d,

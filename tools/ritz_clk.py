@@ -4,7 +4,7 @@ import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2109_03709_b200 as P
 from inputs import configs as C, generate as G
-lib = P.load(); lib.ppca_debug_wait_counters.argtypes = [ctypes.c_void_p]
+lib = P.load(os.environ["PPCA_EXP_LIB"]) if os.environ.get("PPCA_EXP_LIB") else P.load(); lib.ppca_debug_wait_counters.argtypes = [ctypes.c_void_p]
 w = C.SMALL["C3s"]; s = w.spec
 ctx = P.ppca_ctx_create(0, torch.cuda.current_stream())
 X = torch.from_numpy(np.ascontiguousarray(G.dataset(s), dtype=np.float32)).cuda()
