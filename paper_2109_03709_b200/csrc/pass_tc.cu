@@ -258,8 +258,8 @@ static int persistent_ctas(const Ctx* c) { return c->side_busy ? c->sm_count - 1
 
 // How many 2-CTA clusters of a kernel (dynamic smem, threads) can be resident at once; cached per device in
 // *cache.  The persistent pair kernels deal tiles statically, so a cluster beyond that number would start only
-// when another has finished its whole share: launching more than fit doubles the tail (not every one of the
-// 148 SMs can pair up; C3: 74 clusters 1.02-1.05 ms, 73 clusters 0.885 ms).
+// when another has finished its whole share: launching more than fit would double the tail (a guard for
+// partitioned GPUs and smem carve-outs; on a whole B200 all 74 pairs fit).
 static int max_pair_clusters(Ctx* c, const void* kern, size_t smem, int threads, int* cache) {
   const int dev = c->device & 63;
   if (cache[dev] > 0) return cache[dev];
