@@ -284,11 +284,26 @@ def run_ours(args, w, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- timed region (inputs 4 GB ≫ 126 MB L2: no flush needed)
+    # ---------------- kernel timing: an instrumented region (CUDA events around the pass kernels on the library
+    # stream) of the same K steps; the events would break the programmatic dependent launches of the chain, so
+    # the step time (value) comes from the uninstrumented timed region below
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     P.ppca_set_timing(ctx, True)
     P.ppca_get_pass_time(ctx)
     P.ppca_get_kernel_time(ctx, 0), P.ppca_get_kernel_time(ctx, 1)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    P.ppca_prime_power(ctx, Xm, w.m, args.steps, 0, W, theta_hist=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_prof = max_over_ranks(ev0.elapsed_time(ev1))
+    pass_ms_tot, passes = P.ppca_get_pass_time(ctx)
+    ka_ms_tot, ka_n = P.ppca_get_kernel_time(ctx, 0)      # kernel A: Y = X·W'ᵀ, S = YᵀY (reads X once)
+    kb_ms_tot, kb_n = P.ppca_get_kernel_time(ctx, 1)      # kernel B: Zᵀ = X_hiᵀ·Y
+    P.ppca_set_timing(ctx, False)
+    # ---------------- timed region (inputs 4 GB ≫ 126 MB L2: no flush needed)
     l0 = P.ppca_launch_count(ctx)
     k0 = P.ppca_collective_count(ctx)
     with ClockSampler(local_rank) as clk:
@@ -303,10 +318,6 @@ def run_ours(args, w, rank, world, local_rank):
         barrier()
     launches = P.ppca_launch_count(ctx) - l0
     collectives = P.ppca_collective_count(ctx) - k0
-    pass_ms_tot, passes = P.ppca_get_pass_time(ctx)
-    ka_ms_tot, ka_n = P.ppca_get_kernel_time(ctx, 0)      # kernel A: Y = X·W'ᵀ, S = YᵀY (reads X once)
-    kb_ms_tot, kb_n = P.ppca_get_kernel_time(ctx, 1)      # kernel B: Zᵀ = X_hiᵀ·Y
-    P.ppca_set_timing(ctx, False)
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / args.steps
     bytes_step = s.n * s.d * elt                       # whole job: every rank streams its shard once
@@ -334,12 +345,12 @@ def run_ours(args, w, rank, world, local_rank):
     if kernels and len(kernels) == 1:                  # the single-read fused kernel is the pass
         kname, k_tot, k_n, k_bytes = kernels[0]
         k_ms = max_over_ranks(k_tot / k_n)
-        kernel_share = k_tot / max(ms, 1e-9)
+        kernel_share = k_tot / max(ms_prof, 1e-9)
     else:                                              # two kernels (X read twice) or SIMT: the whole pass, vs
         kname = (f"power pass ({' + '.join(k[0].split()[0] for k in kernels)} + reductions; X read twice)"
                  if kernels else f"streaming pass ({plan_impl})")
         k_ms, k_n, k_bytes = pass_ms, passes, per_rank_bytes          # ONE read of X (algorithmic bytes)
-        kernel_share = pass_ms_tot / max(ms, 1e-9)
+        kernel_share = pass_ms_tot / max(ms_prof, 1e-9)
     achieved = k_bytes / (k_ms / 1e3) / 1e9
     # the contraction's own roofline (context): algorithmic 4·n·d·m flop per power pass against the measured
     # bf16 dense peak (burst: the kernels are timed inside the step's sequence, not back to back for seconds)
@@ -519,8 +530,16 @@ def run_minibatch(args, w, rank, world, local_rank):
         return float(t.item())
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # kernel times from an instrumented run of the same steps (the events around the window-pass kernels break
+    # the programmatic dependent launches of the step: ≈ 25 µs per C4 step), the step time uninstrumented
     P.ppca_set_timing(ctx, True)
     P.ppca_get_pass_time(ctx), P.ppca_get_kernel_time(ctx, 0), P.ppca_get_kernel_time(ctx, 1)
+    step0 = fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, steps, 0, V, vel, step0)
+    torch.cuda.synchronize()
+    pass_ms_tot, passes = P.ppca_get_pass_time(ctx)
+    ka_ms, ka_n = P.ppca_get_kernel_time(ctx, 0)
+    kb_ms, kb_n = P.ppca_get_kernel_time(ctx, 1)
+    P.ppca_set_timing(ctx, False)
     l0 = P.ppca_launch_count(ctx)
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -531,10 +550,6 @@ def run_minibatch(args, w, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
     launches = P.ppca_launch_count(ctx) - l0
-    pass_ms_tot, passes = P.ppca_get_pass_time(ctx)
-    ka_ms, ka_n = P.ppca_get_kernel_time(ctx, 0)
-    kb_ms, kb_n = P.ppca_get_kernel_time(ctx, 1)
-    P.ppca_set_timing(ctx, False)
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / steps
     batch_bytes = w.batch * s.d * 4

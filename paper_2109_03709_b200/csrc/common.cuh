@@ -282,7 +282,14 @@ __device__ __forceinline__ double sum_in_order(int64_t begin, int64_t end, int64
 #pragma unroll
     for (int u = 0; u < U; ++u) s += v[u];
   }
-  for (; i < end; i += step) s += load(i);
+  if (i < end) {                                  // the tail as one more batch (loads in flight together)
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = i + u * step < end ? load(i + u * step) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * step < end) s += v[u];           // same order as the loop it replaces
+  }
   return s;
 }
 

@@ -330,6 +330,9 @@ def test_refine_sampled_parity_c3s(P, ctx, impl, fraction):
     assert err < 1e-4
     gi = U.gapped(th_ref, w.k)
     assert U.abs_cos(E.cpu().numpy()[gi], E_ref[gi]).min() >= 0.9999
+    l_gpu, _ = U.lces_all(E.cpu().numpy(), T[: w.k])          # the paper's measure (P L411-413): identical
+    l_ref, _ = U.lces_all(E_ref, T[: w.k])
+    assert l_gpu == l_ref, f"sampled refine LCES {l_gpu} vs oracle {l_ref}"
 
 
 # ----------------------------------------------------------------------------- refine edge cases
