@@ -557,8 +557,21 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   // pre-touch the scratch the loop uses so no allocation happens while the side stream is busy
   if (!scratch(c, S_EVAL, (size_t)3 * m * m * sizeof(double)) || !scratch(c, S_GRAM, (size_t)2 * m * m * sizeof(double)) ||
       !scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64) ||
-      !scratch(c, S_W2, (size_t)m * d * sizeof(float)) || !scratch(c, S_SIDE_PART, vec_gram_part_bytes(c, m, d)))
+      !scratch(c, S_W2, (size_t)m * d * sizeof(float)) || !scratch(c, S_SIDE_PART, vec_gram_part_bytes(c, m, d)) ||
+      !scratch(c, S_ZGRAM, zgram_part_bytes(m, d)))
     return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  // the next pass operand W' written by CholQR's apply (small d·m, one rank's replicated CholQR): two buffers —
+  // the apply of iteration t writes wp_buf[t & 1] while the side Gram of iteration t may still read the other
+  const int mp_op = (m + 15) & ~15;
+  const bool fuse_prep = plan.impl == 2 && oblk == 0 && wprep_fusable(c, m, mp_op, d);
+  const size_t wp_bytes = (size_t)2 * mp_op * d * 2 + (size_t)m * d * 4 + 256;
+  uint8_t* wp_buf[2] = {nullptr, nullptr};
+  if (fuse_prep) {
+    wp_buf[0] = (uint8_t*)scratch(c, S_WPREP, wp_bytes);
+    wp_buf[1] = (uint8_t*)scratch(c, S_TC1, wp_bytes);   // prep_w's own buffer (pass 0)
+    if (!wp_buf[0] || !wp_buf[1]) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+  }
+  c->wprep_for = nullptr;
   cudaEvent_t ev_main[2], ev_side[2], ev_prep, ev_gram;
   cudaEventCreateWithFlags(&ev_prep, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ev_gram, cudaEventDisableTiming);
@@ -585,7 +598,12 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
       cudaStreamWaitEvent(c->stream, ev_gram, 0);          // the side Gram of W'_{t-1} read it before prep_w rewrites
     }
     c->z_block_cols = oblk > 0 ? d / oblk : 0;               // the pass writes Z d-blocked for the slices
+    // one rank, replicated CholQR: the pass's Z reduction may also leave the CholQR's Gram ZᵀZ
+    c->zgram_want = oblk == 0 && c->nccl_comm == nullptr;
+    c->zgram_done = false;
     st = pass_power(c, X, &plan, W, m, Z, S);               // Z = YᵀX, S = YᵀY  (local)
+    const bool gram_ready = c->zgram_done;
+    c->zgram_want = c->zgram_done = false;
     c->z_block_cols = 0;
     if (st != PPCA_OK) break;
     if (theta_hist_host) {
@@ -621,8 +639,21 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
                       "keep W_t");
       if (st != PPCA_OK) break;
     }
-    st = oblk > 0 ? cholqr_dist(c, Z, Zg, W, m, d, oblk) : cholqr(c, Z, W, m, d, 0.0, nullptr, 1);
+    WPrep wp{};
+    if (fuse_prep) {
+      uint8_t* b = wp_buf[t & 1];
+      wp.Wb = reinterpret_cast<__nv_bfloat16*>(b);
+      wp.Wr = reinterpret_cast<float*>(b + (((size_t)2 * mp_op * d * 2 + 255) & ~(size_t)255));
+      wp.lo_off = (int64_t)mp_op * d;
+    }
+    st = oblk > 0 ? cholqr_dist(c, Z, Zg, W, m, d, oblk)
+                  : cholqr(c, Z, W, m, d, 0.0, nullptr, 1, gram_ready, fuse_prep ? &wp : nullptr);
     if (st != PPCA_OK) break;
+    if (fuse_prep) {
+      c->wprep_for = W;
+      c->wprep_b = wp.Wb;
+      c->wprep_r = wp.Wr;
+    }
     done = t + 1;
     if (stop_rule) {                                 // P L61-62: stop once every column moved less than eps
       st = row_dots(c, W, Wold, m, d, dots);
@@ -637,6 +668,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
     }
   }
   c->prep_ev = nullptr;
+  c->wprep_for = nullptr;
   c->side_busy = false;
   if (c->s_pending) pass_reduce_deferred_s(c, Sbuf, c->side);   // an aborted loop: drain (result unused)
   ppca_status st2 = finish(c, "ppca_prime_power");

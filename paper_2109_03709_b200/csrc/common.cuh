@@ -67,6 +67,14 @@ struct Ctx {
   // distributed CholQR (§6): 0 = auto, 1 = replicated, b ≥ 2 = d-slices (world == 1: b emulated slices, tests)
   int orth_split = 0;
   int64_t z_block_cols = 0;           // > 0: the pass writes Z d-blocked [d/z_block_cols][m][z_block_cols]
+  // power loop on one rank (no later all-reduce of Z): the pass may also leave G = ZᵀZ (fp64, S_GRAM) for the
+  // CholQR that follows (zgram_want: allowed; zgram_done: it did)
+  bool zgram_want = false;
+  bool zgram_done = false;
+  // power loop: CholQR's apply already wrote the next pass operand W' of W = wprep_for (prep_w adopts it)
+  const float* wprep_for = nullptr;
+  __nv_bfloat16* wprep_b = nullptr;
+  float* wprep_r = nullptr;
   // pass timing (bench): event pairs recorded around each pass
   bool timing = false;
   std::vector<cudaEvent_t> tev;
@@ -104,6 +112,8 @@ enum Slot {
   S_EPS,                           // power stop rule: W_t copy + column dots
   S_DIST,                          // distributed CholQR: this rank's Z slice and W slice
   S_SIGN,                          // sign convention partials of very long rows
+  S_ZGRAM,                         // cluster partials of the pass's Gram of Z (reduce_zp_gram)
+  S_WPREP,                         // the power loop's second W' buffer (written by CholQR's apply)
 };
 
 void* scratch(Ctx* c, int slot, size_t bytes);     // grow-only, device memory

@@ -35,6 +35,7 @@ ppca_status ytx(Ctx* c, const ppca_matrix* X, int64_t r0, int64_t rows, const fl
 ppca_status yty(Ctx* c, const float* Y, int m, int64_t rows, double* S);
 
 // the fused pass's deferred S reduction (Ctx::s_defer) on stream st; no-op when nothing is pending
+size_t zgram_part_bytes(int m, int64_t d);   // scratch S_ZGRAM of the power pass's fused Z Gram
 ppca_status pass_reduce_deferred_s(Ctx* c, double* S, cudaStream_t st);
 
 }  // namespace ppca

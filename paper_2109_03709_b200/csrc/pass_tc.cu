@@ -236,6 +236,106 @@ __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict_
   }
 }
 
+// The Z reduction of the power pass with the Gram of the CholQR that follows folded in (one rank, m ≤ 64, d-major
+// Z): a CTA owns ZG_X = 2 features x and every component j.  Z is summed exactly as reduce_zp_cols_kernel sums
+// it (sub-sum w over the row groups g ≡ w mod 8 in order, then the 8 sub-sums in w order: the same bits; 16
+// loads in flight per thread — the sum is L2-latency bound, so it needs many CTAs and many loads in flight).
+// The 8 CTAs of a cluster then gather their 16 rows of Z through distributed shared memory and each computes
+// one eighth of the cluster's Gram partial Σ_x z_x z_xᵀ (fp64 of the stored fp32 values, x ascending) — one
+// m×m partial per cluster, summed in cluster order by reduce_splits.  Replaces vec_gram's two launches on the
+// Z the pass has just produced (15.8 + 1.9 µs for C3).
+constexpr int ZG_X = 2, ZG_CL = 8, ZG_B = 4;
+__global__ void __launch_bounds__(256) reduce_zp_gram_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
+                                                             int mp, int m, int64_t d, float* __restrict__ Z,
+                                                             double* __restrict__ Gpart) {
+  pdl_enter();
+  __shared__ double part[8][ZG_X * 64];
+  __shared__ __align__(16) float zf[ZG_X * 64];
+  __shared__ __align__(16) float zall[ZG_CL * ZG_X * 64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t x0 = (int64_t)blockIdx.x * ZG_X;
+  const int j0 = lane, j1 = lane + 32;
+  double acc[ZG_X][2];
+#pragma unroll
+  for (int xi = 0; xi < ZG_X; ++xi) acc[xi][0] = acc[xi][1] = 0.0;
+  const float* base[ZG_X];
+#pragma unroll
+  for (int xi = 0; xi < ZG_X; ++xi) base[xi] = Zp + min(x0 + xi, d - 1) * mp;
+  const int64_t gstride = dpad * mp;
+  for (int64_t g0 = warp; g0 < nrg; g0 += 8 * ZG_B) {
+    float v[ZG_B][ZG_X][2];
+#pragma unroll
+    for (int u = 0; u < ZG_B; ++u) {
+      const int64_t g = g0 + 8 * u;
+#pragma unroll
+      for (int xi = 0; xi < ZG_X; ++xi) {
+        const float* src = base[xi] + min(g, nrg - 1) * gstride;
+        v[u][xi][0] = j0 < m ? src[j0] : 0.f;
+        v[u][xi][1] = j1 < m ? src[j1] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ZG_B; ++u)
+      if (g0 + 8 * u < nrg) {
+#pragma unroll
+        for (int xi = 0; xi < ZG_X; ++xi) {
+          acc[xi][0] += (double)v[u][xi][0];
+          acc[xi][1] += (double)v[u][xi][1];
+        }
+      }
+  }
+#pragma unroll
+  for (int xi = 0; xi < ZG_X; ++xi) {
+    part[warp][xi * 64 + j0] = acc[xi][0];
+    part[warp][xi * 64 + j1] = acc[xi][1];
+  }
+  __syncthreads();
+  if (threadIdx.x < ZG_X * 64) {
+    const int e = threadIdx.x, xi = e / 64, j = e % 64;
+    const int64_t x = x0 + xi;
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][e];
+    const float zv = (float)t;
+    const bool live = x < d && j < m;
+    zf[e] = live ? zv : 0.f;
+    if (live) Z[(int64_t)j * d + x] = zv;
+  }
+  cluster_barrier();                             // every CTA's rows of Z are in its shared memory
+  if (threadIdx.x < ZG_CL * ZG_X * 64 / 4) {       // gather the cluster's 16 rows (rank order = x order)
+    const int r = threadIdx.x / (ZG_X * 16), o = threadIdx.x % (ZG_X * 16);
+    uint32_t ra, a, b, c2, e2;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(ra)
+                 : "r"((uint32_t)__cvta_generic_to_shared(zf) + (uint32_t)o * 16u), "r"(r));
+    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c2), "=r"(e2) : "r"(ra));
+    *reinterpret_cast<uint4*>(&zall[r * ZG_X * 64 + o * 4]) = make_uint4(a, b, c2, e2);
+  }
+  cluster_barrier();                             // every gather is done before any CTA may exit
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int mm = m * m, per = (mm + ZG_CL - 1) / ZG_CL;
+  const int e0 = (int)rank * per, e1 = min(mm, e0 + per);
+  double* out = Gpart + (int64_t)(blockIdx.x / ZG_CL) * mm;
+  for (int e = e0 + threadIdx.x; e < e1; e += 256) {
+    const int i = e / m, j = e % m;
+    double t = 0.0;
+#pragma unroll
+    for (int x = 0; x < ZG_CL * ZG_X; ++x) t = fma((double)zall[x * 64 + i], (double)zall[x * 64 + j], t);
+    out[e] = t;
+  }
+}
+
+size_t zgram_part_bytes(int m, int64_t d) {
+  return (size_t)ceil_div(ceil_div(d, (int64_t)ZG_X), (int64_t)ZG_CL) * m * m * sizeof(double);
+}
+
+// number of cluster partials reduce_zp_gram leaves (0: not applicable)
+static int zgram_parts(int64_t nrg, int m, int64_t d, int64_t ds) {
+  if (nrg <= 16 || m > 64 || ds != d) return 0;
+  return (int)ceil_div(ceil_div(d, (int64_t)ZG_X), (int64_t)ZG_CL);
+}
+
 static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad, int mp, int m, int64_t d, float* Z) {
   const int64_t ds = c->z_block_cols > 0 ? c->z_block_cols : d;
   if (nrg > 16)
@@ -412,6 +512,12 @@ ppca_status pass_tc_prepare(Ctx* c, const ppca_matrix* X, int m, PassPlan* plan)
 
 // W' (bf16 + its fp32 value copy) → S_TC1;  returns pointers
 static ppca_status prep_w(Ctx* c, const float* W, int m, int mp, int64_t d, __nv_bfloat16** Wb, float** Wr) {
+  if (c->wprep_for == W && W) {                   // CholQR's apply wrote this W's operand already
+    *Wb = c->wprep_b;
+    *Wr = c->wprep_r;
+    c->wprep_for = nullptr;
+    return PPCA_OK;
+  }
   uint8_t* buf = (uint8_t*)scratch(c, S_TC1, (size_t)2 * mp * d * 2 + (size_t)m * d * 4 + 256);
   if (!buf) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
   *Wb = reinterpret_cast<__nv_bfloat16*>(buf);
@@ -850,6 +956,8 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
   KP2Params pp;
   pp.n = n; pp.d = d; pp.ntiles = ntiles; pp.nrg = nrg; pp.tiles_per_rg = tpr;
   pp.Spart = Spart; pp.Zp = Zp; pp.trace = nullptr;
+  static const int pair_pol = tune_env("PPCA_PAIR_POL", 0 | 2 << 2 | 2 << 4);   // hi evict_last, lo / re-read evict_first
+  pp.pol = pair_pol;
 #ifdef PPCA_EXPERIMENTS
   static int trace_at = -1, launches = 0;         // PPCA_TRACE=k: stamp the k-th launch, dump it to gpurun_out/
   if (trace_at < 0) trace_at = tune_env("PPCA_TRACE", 0);
@@ -890,6 +998,31 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
   } else {
     launch_pdl(reduce_spart2_kernel, dim3((unsigned)ceil_div(m * m, 32)), dim3(256), 0, c->stream, Spart, grid, mp, m, S);
     PPCA_LAUNCH_CHECK(c, "reduce_spart");
+  }
+  const int ngp = c->zgram_want ? zgram_parts(nrg, m, d, c->z_block_cols > 0 ? c->z_block_cols : d) : 0;
+  if (ngp > 0) {                                  // Z and its Gram (the CholQR's) in one launch
+    double* Gp = (double*)scratch(c, S_ZGRAM, (size_t)ngp * m * m * sizeof(double));
+    double* G = (double*)scratch(c, S_GRAM, (size_t)m * m * sizeof(double));
+    if (!Gp || !G) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ngp * ZG_CL));
+    cfg.blockDim = dim3(256);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ZG_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 2 : 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, reduce_zp_gram_kernel, (const float*)Zp, nrg, dpad, mp, m, d, Z, Gp);
+    if (le != cudaSuccess) return check_cuda(c, le, "reduce_zp_gram");
+    PPCA_LAUNCH_CHECK(c, "reduce_zp_gram");
+    PPCA_TRY(launch_reduce_splits_f64(c, Gp, ngp, (int64_t)m * m, G, c->stream));
+    c->zgram_done = true;
+    return PPCA_OK;
   }
   launch_reduce_zp(c, Zp, nrg, dpad, mp, m, d, Z);
   PPCA_LAUNCH_CHECK(c, "reduce_zp");

@@ -648,7 +648,9 @@ constexpr int AP_COLS = 32;
 __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
                                                          int m_in, const int* __restrict__ row_map,
                                                          bool lower, const float* __restrict__ IN,
-                                                         int64_t d, float* __restrict__ OUT, int rows_per_cta) {
+                                                         int64_t d, float* __restrict__ OUT, int rows_per_cta,
+                                                         __nv_bfloat16* __restrict__ Wb, float* __restrict__ Wr,
+                                                         int64_t lo_off) {
   pdl_enter();
   extern __shared__ double cs[];                 // this CTA's rows × m_in (fp64), then m_in × AP_COLS (fp32)
   const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
@@ -680,20 +682,31 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
       a3 = fma(crow[j + 3], (double)ins[(j + 3) * AP_COLS + lane], a3);
     }
     for (; j < jend; ++j) a0 = fma(crow[j], (double)ins[j * AP_COLS + lane], a0);
-    if (x < d) OUT[(int64_t)oi * d + x] = (float)((a0 + a1) + (a2 + a3));
+    if (x < d) {
+      const float o = (float)((a0 + a1) + (a2 + a3));
+      const int64_t e = (int64_t)oi * d + x;
+      OUT[e] = o;
+      if (Wb) {                                   // the next pass's operand, as prep_w_kernel splits it
+        const __nv_bfloat16 h = __float2bfloat16_rn(o);
+        const float hf = __bfloat162float(h);
+        const __nv_bfloat16 l = __float2bfloat16_rn(o - hf);
+        Wb[e] = h;
+        Wb[lo_off + e] = l;
+        Wr[e] = hf + __bfloat162float(l);
+      }
+    }
   }
 }
 
 static ppca_status apply_rows_small(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
-                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st,
+                              const WPrep* prep = nullptr) {
+  static uint64_t attr = 0;
+  if (first_on_device(&attr, c->device))
     cudaFuncSetAttribute(apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
   // row blocks (multiples of 8 rows) until the grid covers the SMs: d = 1024 alone gives 32 CTAs
   const int64_t gx = ceil_div(d, (int64_t)AP_COLS);
-  static const bool split = !(getenv("PPCA_APPLY_SPLIT") && atoi(getenv("PPCA_APPLY_SPLIT")) == 0);
+  static const bool split = tune_env("PPCA_APPLY_SPLIT", 1) != 0;
   int rpc = rows;
   if (split && gx < c->sm_count) {
     const int gy = (int)std::min<int64_t>(ceil_div((int64_t)c->sm_count, gx), ceil_div((int64_t)rows, (int64_t)8));
@@ -701,7 +714,8 @@ static ppca_status apply_rows_small(Ctx* c, const double* C, int ldc, int rows, 
   }
   const unsigned gy = (unsigned)ceil_div((int64_t)rows, (int64_t)rpc);
   size_t smem = (size_t)rpc * m_in * sizeof(double) + (size_t)m_in * AP_COLS * sizeof(float);
-  launch_pdl(apply_rows_kernel, dim3(dim3((unsigned)gx, gy)), dim3(256), smem, st, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc);
+  launch_pdl(apply_rows_kernel, dim3(dim3((unsigned)gx, gy)), dim3(256), smem, st, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, rpc,
+             prep ? prep->Wb : nullptr, prep ? prep->Wr : nullptr, prep ? prep->lo_off : (int64_t)0);
   PPCA_LAUNCH_CHECK(c, "apply_rows");
   return PPCA_OK;
 }
@@ -824,12 +838,18 @@ static void launch_apply_tiled(Ctx* c, const double* C, int ldc, int rows, int m
   launch_pdl(apply_tiled_kernel<RPT>, dim3(grid), dim3(256), smem, st, C, ldc, rows, m_in, row_map, lower, IN, d, OUT);
 }
 
+static bool apply_small(const Ctx* c, int64_t d) { return ceil_div(d, (int64_t)AT_COLS) < 2 * c->sm_count; }
+
+bool wprep_fusable(const Ctx* c, int m, int mp, int64_t d) { return m == mp && m <= 128 && apply_small(c, d); }
+
 static ppca_status apply_rows(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map,
-                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st) {
+                              bool lower, const float* IN, int64_t d, float* OUT, cudaStream_t st,
+                              const WPrep* prep = nullptr) {
   if (rows < 1 || m_in < 1 || d < 1) return PPCA_OK;
   if (rows > 128 || m_in > 128) return set_error(c, PPCA_ERR_UNSUPPORTED, "apply: %d x %d > 128", rows, m_in);
-  if (ceil_div(d, (int64_t)AT_COLS) < 2 * c->sm_count)
-    return apply_rows_small(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
+  if (apply_small(c, d))
+    return apply_rows_small(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st, prep);
+  if (prep) return set_error(c, PPCA_ERR_UNSUPPORTED, "apply: fused operand split needs the short-d kernel");
   if (rows <= 32) launch_apply_tiled<1>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   else if (rows <= 64) launch_apply_tiled<2>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
   else launch_apply_tiled<4>(c, C, ldc, rows, m_in, row_map, lower, IN, d, OUT, st);
@@ -866,7 +886,8 @@ ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_
 // W = Q-factor of the rows of Zin (positive diag R).  One pass is exact up to ε64·κ(Zin)² in fp64
 // (the Gram, Cholesky and apply are fp64); a second pass restores orthonormality for ill-conditioned
 // inputs (the refine path).
-ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes) {
+ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes,
+                   bool gram_ready, const WPrep* prep) {
   double* G = (double*)scratch(c, S_GRAM, (size_t)m * m * sizeof(double));
   double* Linv = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + 2 * m * sizeof(int) + 64);
   int* row_map = (int*)(Linv + (size_t)m * m);
@@ -879,16 +900,17 @@ ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double 
   }
   const size_t smem = chol_inv_smem(m);
   if (Zin != W && passes == 1 && drop_tol <= 0.0) {
-    PPCA_TRY(vec_gram(c, Zin, m, d, G));
+    if (!gram_ready) PPCA_TRY(vec_gram(c, Zin, m, d, G));
     if (m <= 2 * CF_M && g_chol_reg)
       launch_chol_inv_reg(G, m, Linv, row_map, d_mout, c->d_err, c->stream);
     else
       launch_pdl(chol_inv_kernel, dim3(1), dim3(256), smem, c->stream, G, m, 0.0, Linv, row_map, d_mout, c->d_err);
     PPCA_LAUNCH_CHECK(c, "chol_inv");
-    PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, Zin, d, W, c->stream));
+    PPCA_TRY(apply_rows(c, Linv, m, m, m, nullptr, true, Zin, d, W, c->stream, prep));
     if (m_out) *m_out = m;
     return PPCA_OK;
   }
+  if (prep) return set_error(c, PPCA_ERR_UNSUPPORTED, "cholqr: fused operand split on the one-pass path only");
   if (Zin != W)
     PPCA_TRY(check_cuda(c, cudaMemcpyAsync(W, Zin, (size_t)m * d * sizeof(float), cudaMemcpyDeviceToDevice, c->stream),
                         "copy Z"));

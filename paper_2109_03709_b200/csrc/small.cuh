@@ -21,7 +21,18 @@ ppca_status apply_lower_on(Ctx* c, const double* L, int m, const float* IN, int6
 // drop_tol == 0: any non-positive pivot flags SUBSPACE_COLLAPSE (power-iteration semantics).
 ppca_status cholqr2(Ctx* c, float* W, int m, int64_t d, double drop_tol, int* m_out);
 // General form: W (may alias Zin) = orth(Zin) with `passes` Cholesky-QR passes.
-ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes);
+// The power loop's next pass operand W' = [W_hi; W_lo] (bf16 rows hi = RN(W), lo = RN(W − hi), lo rows at
+// lo_off elements) and Wr = hi + lo, written by CholQR's apply together with W (what prep_w would compute
+// from W, bit for bit) when wprep_fusable(): one launch fewer per power iteration.
+struct WPrep {
+  __nv_bfloat16* Wb;
+  float* Wr;
+  int64_t lo_off;
+};
+bool wprep_fusable(const Ctx* c, int m, int mp, int64_t d);
+// gram_ready: the S_GRAM scratch already holds ZinᵀZin (the power pass's reduce_zp_gram; one pass, no drops)
+ppca_status cholqr(Ctx* c, const float* Zin, float* W, int m, int64_t d, double drop_tol, int* m_out, int passes,
+                   bool gram_ready = false, const WPrep* prep = nullptr);
 
 // Rayleigh–Ritz in one CTA (fp64): given S = (XWᵀ)ᵀ(XWᵀ) and Bm = WWᵀ of the operand rows,
 // solve S u = θ Bm u:  L = chol(Bm), Jacobi(L⁻¹SL⁻ᵀ) → θ (desc), U;  R = Uᵀ L⁻¹.

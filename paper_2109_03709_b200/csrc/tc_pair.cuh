@@ -42,6 +42,7 @@ struct KP2Params {
   int64_t tiles_per_rg;          // row group r: tiles [r·tpr, min(ntiles, (r+1)·tpr))
   double* Spart;                 // [grid][2·MP][MP]
   float* Zp;                     // [nrg][2·SL][MP]
+  int pol;                       // L2 policies (policy_sel codes): A-stream hi | lo << 2 | product-2 re-read << 4
   long long* trace;              // experiment builds only: per-tile clock64 stamps of cluster 0 (nullptr: off)
 };
 
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kp2::NTHREADS, 1)
     if (lane == 0) {
       // the L2 producer: W' chunks (product 1) and the X_hi slice stages of product 2, polled round-robin so
       // that neither ring waits behind the other (both are L2 hits; W' first: it gates the HBM stream)
-      const uint64_t drop = policy_evict_first();
+      const uint64_t drop = policy_sel((p.pol >> 4) & 3);
       const int nbl = 2 * mc;
       const int64_t nw = ntl * nk, nq = ntl * BPT;
       int64_t iw = 0, q = 0;
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(kp2::NTHREADS, 1)
   } else if (warp == W_XPROD) {
     if (lane == 0) {
       // the hi plane is re-read by this CTA's product 2 a few µs later (evict_last); the lo plane is read once
-      const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+      const uint64_t keep = policy_sel(p.pol & 3), drop = policy_sel((p.pol >> 2) & 3);
       uint32_t it = 0;
       for (int64_t i = 0; i < ntl; ++i) {
         const int64_t t = tb + i;

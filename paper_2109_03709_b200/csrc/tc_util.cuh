@@ -109,6 +109,22 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 0 evict_last, 1 evict_normal, 2 evict_first, 3 evict_unchanged
+__device__ __forceinline__ uint64_t policy_sel(int k) {
+  return k == 0 ? policy_evict_last() : k == 1 ? policy_evict_normal() : k == 2 ? policy_evict_first()
+                                                                         : policy_evict_unchanged();
+}
+
 // L2 prefetch of the line holding p (no register, no scoreboard: converters run it several chunks ahead
 // of their loads so those hit L2 instead of waiting a full DRAM latency)
 __device__ __forceinline__ void prefetch_l2(const void* p) {
