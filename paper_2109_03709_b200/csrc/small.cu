@@ -534,12 +534,105 @@ __device__ void chol_inv_sweep(const double* __restrict__ G, int m, double* __re
   __syncthreads();
 }
 
+// The same elimination two steps per barrier (steps j and j+1 from columns j, j+1 of A and rows j, j+1 of M as
+// they stand before step j): every thread forms column j+1 and row j+1 after step j itself — with the operation
+// order of the one-step sweep, so the result is bitwise the same — and applies both updates:
+//   p1 = A_{j+1,j+1} − h·A_{j+1,j} (h = A_{j+1,j}/p0),  c1'_i = A_{i,j+1} − (A_ij/p0)·A_{j+1,j},
+//   A_ik −= (A_ij/p0)·A_kj + (c1'_i/p1)·c1'_k  (i, k > j+1),
+//   M_i· −= F0_i·M_j·, then −= F1_i·(M_{j+1}· − h·M_j·)  (F0_j = 1 − r0, F1_{j+1} = 1 − r1, the rest as above).
+// Half the barriers and publications of chol_inv_sweep; the two rsqrt stay sequential.
+template <int CQ>
+__device__ void chol_inv_sweep2(const double* __restrict__ G, int m, double* __restrict__ Linv, int ldl, int* d_err) {
+  static_assert(CQ >= 2, "columns j and j+1 have different owners");
+  __shared__ double colb[2][2][CF_M];
+  __shared__ double rowb[2][2][CF_M];
+  constexpr int NQ = CF_M / CQ;
+  const int t = threadIdx.x, i = t / CQ, cp = t % CQ;
+  double a[NQ], mm_[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int k = cp + CQ * q;
+    a[q] = (i < m && k < m) ? G[i * m + k] : (i == k ? 1.0 : 0.0);
+    mm_[q] = i == k ? 1.0 : 0.0;
+  }
+  if (cp == 0) colb[0][0][i] = a[0];
+  if (cp == 1) colb[0][1][i] = a[0];
+  if (i < 2) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) rowb[0][i][cp + CQ * q] = mm_[q];
+  }
+  __syncthreads();
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CF_M; j += 2) {
+    const int b = (j >> 1) & 1;
+    const double p0 = colb[b][0][j];
+    const double c0j1 = colb[b][0][j + 1];
+    const double c1j1 = colb[b][1][j + 1];
+    const double c0i = colb[b][0][i], c1i = colb[b][1][i];
+    const bool ok0 = p0 > 0.0 && isfinite(p0);
+    const double r0 = ok0 ? rsqrt(p0) : 0.0;
+    const double g0 = r0 * r0;
+    const double h = c0j1 * g0;
+    const double p1 = fma(-h, c0j1, c1j1);
+    const bool ok1 = p1 > 0.0 && isfinite(p1);
+    const double r1 = ok1 ? rsqrt(p1) : 0.0;
+    const double g1 = r1 * r1;
+    bad |= !ok0 || !ok1;
+    const double f0 = c0i * g0;
+    const double c1pi = fma(-f0, c0j1, c1i);
+    const double F0 = i == j ? 1.0 - r0 : f0;
+    const double F1 = i == j + 1 ? 1.0 - r1 : (i > j + 1 ? c1pi * g1 : 0.0);
+    const bool live = i > j + 1;
+    const double fa0 = live ? f0 : 0.0, fa1 = live ? c1pi * g1 : 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = cp + CQ * q;
+      if (CQ * q + CQ - 1 >= j + 2) {             // columns k ≥ j+2 of A
+        const double c0k = colb[b][0][kk];
+        const double c1k = fma(-(c0k * g0), c0j1, colb[b][1][kk]);
+        a[q] = fma(-fa0, c0k, a[q]);
+        a[q] = fma(-fa1, c1k, a[q]);
+      }
+      if (CQ * q <= j + 1) {                      // rows j, j+1 of M have entries k ≤ j+1 only
+        const double mj = rowb[b][0][kk];
+        const double mj1 = fma(-h, mj, rowb[b][1][kk]);
+        mm_[q] = fma(-F0, mj, mm_[q]);
+        mm_[q] = fma(-F1, mj1, mm_[q]);
+      }
+    }
+    if (j + 2 < CF_M) {                          // publish columns j+2, j+3 of A and rows j+2, j+3 of M
+      const int jn = j + 2, nb = b ^ 1;
+      if (cp == jn % CQ) colb[nb][0][i] = i >= jn ? a[jn / CQ] : 0.0;
+      if (cp == (jn + 1) % CQ) colb[nb][1][i] = i >= jn ? a[(jn + 1) / CQ] : 0.0;
+      if (i == jn || i == jn + 1) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (CQ * q <= jn + 1) rowb[nb][i - jn][cp + CQ * q] = mm_[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && t == 0) atomicOr(d_err, DEV_COLLAPSE);
+  if (i < m) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = cp + CQ * q;
+      if (k < m) Linv[i * ldl + k] = mm_[q];
+    }
+  }
+  __syncthreads();
+}
+
+static const bool g_chol2 = tune_env("PPCA_CHOL2", 1) != 0;
+
 template <int CQ>
 __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
                                                            double* __restrict__ Linv, int* __restrict__ row_map,
-                                                           int* __restrict__ m_out, int* d_err) {
+                                                           int* __restrict__ m_out, int* d_err, bool two_step) {
   pdl_enter();
-  chol_inv_sweep<CQ>(G, m, Linv, m, nullptr, d_err);
+  if (two_step) chol_inv_sweep2<CQ>(G, m, Linv, m, d_err);
+  else chol_inv_sweep<CQ>(G, m, Linv, m, nullptr, d_err);
   if (threadIdx.x < m) row_map[threadIdx.x] = threadIdx.x;
   if (threadIdx.x == 0) *m_out = m;
 }
@@ -623,11 +716,11 @@ static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_m
     return;
   }
   if (g_chol_cq == 4)
-    launch_pdl(chol_inv_reg_kernel<4>, dim3(1), dim3(256), 0, st, G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<4>, dim3(1), dim3(256), 0, st, G, m, Linv, row_map, m_out, d_err, g_chol2);
   else if (g_chol_cq == 16)
-    launch_pdl(chol_inv_reg_kernel<16>, dim3(1), dim3(1024), 0, st, G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<16>, dim3(1), dim3(1024), 0, st, G, m, Linv, row_map, m_out, d_err, g_chol2);
   else
-    launch_pdl(chol_inv_reg_kernel<8>, dim3(1), dim3(512), 0, st, G, m, Linv, row_map, m_out, d_err);
+    launch_pdl(chol_inv_reg_kernel<8>, dim3(1), dim3(512), 0, st, G, m, Linv, row_map, m_out, d_err, g_chol2);
 }
 
 static size_t chol_inv_smem(int m) {
