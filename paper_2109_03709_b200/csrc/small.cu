@@ -624,14 +624,109 @@ __device__ void chol_inv_sweep2(const double* __restrict__ G, int m, double* __r
   __syncthreads();
 }
 
-static const bool g_chol2 = tune_env("PPCA_CHOL2", 1) != 0;
+// chol_inv_sweep2 with the two published columns (and the two M rows) interleaved as double2: one 16-byte
+// shared load gives a thread both operands of a column index (the sweep is bound by its shared-memory loads:
+// every thread reads the published column and row at its 2·64/CQ indices each step).  Bitwise the same result.
+template <int CQ>
+__device__ void chol_inv_sweep2p(const double* __restrict__ G, int m, double* __restrict__ Linv, int ldl, int* d_err) {
+  static_assert(CQ >= 2, "columns j and j+1 have different owners");
+  __shared__ double2 colb[2][CF_M];
+  __shared__ double2 rowb[2][CF_M];
+  constexpr int NQ = CF_M / CQ;
+  const int t = threadIdx.x, i = t / CQ, cp = t % CQ;
+  double a[NQ], mm_[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int k = cp + CQ * q;
+    a[q] = (i < m && k < m) ? G[i * m + k] : (i == k ? 1.0 : 0.0);
+    mm_[q] = i == k ? 1.0 : 0.0;
+  }
+  if (cp == 0) colb[0][i].x = a[0];
+  if (cp == 1) colb[0][i].y = a[0];
+  if (i < 2) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (i == 0) rowb[0][cp + CQ * q].x = mm_[q];
+      else rowb[0][cp + CQ * q].y = mm_[q];
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CF_M; j += 2) {
+    const int b = (j >> 1) & 1;
+    const double p0 = colb[b][j].x;
+    const double2 cj1 = colb[b][j + 1];
+    const double c0j1 = cj1.x, c1j1 = cj1.y;
+    const double2 ci = colb[b][i];
+    const double c0i = ci.x, c1i = ci.y;
+    const bool ok0 = p0 > 0.0 && isfinite(p0);
+    const double r0 = ok0 ? rsqrt(p0) : 0.0;
+    const double g0 = r0 * r0;
+    const double h = c0j1 * g0;
+    const double p1 = fma(-h, c0j1, c1j1);
+    const bool ok1 = p1 > 0.0 && isfinite(p1);
+    const double r1 = ok1 ? rsqrt(p1) : 0.0;
+    const double g1 = r1 * r1;
+    bad |= !ok0 || !ok1;
+    const double f0 = c0i * g0;
+    const double c1pi = fma(-f0, c0j1, c1i);
+    const double F0 = i == j ? 1.0 - r0 : f0;
+    const double F1 = i == j + 1 ? 1.0 - r1 : (i > j + 1 ? c1pi * g1 : 0.0);
+    const bool live = i > j + 1;
+    const double fa0 = live ? f0 : 0.0, fa1 = live ? c1pi * g1 : 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = cp + CQ * q;
+      if (CQ * q + CQ - 1 >= j + 2) {
+        const double2 ck = colb[b][kk];
+        const double c1k = fma(-(ck.x * g0), c0j1, ck.y);
+        a[q] = fma(-fa0, ck.x, a[q]);
+        a[q] = fma(-fa1, c1k, a[q]);
+      }
+      if (CQ * q <= j + 1) {
+        const double2 mk = rowb[b][kk];
+        const double mj1 = fma(-h, mk.x, mk.y);
+        mm_[q] = fma(-F0, mk.x, mm_[q]);
+        mm_[q] = fma(-F1, mj1, mm_[q]);
+      }
+    }
+    if (j + 2 < CF_M) {
+      const int jn = j + 2, nb = b ^ 1;
+      if (cp == jn % CQ) colb[nb][i].x = i >= jn ? a[jn / CQ] : 0.0;
+      if (cp == (jn + 1) % CQ) colb[nb][i].y = i >= jn ? a[(jn + 1) / CQ] : 0.0;
+      if (i == jn) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (CQ * q <= jn + 1) rowb[nb][cp + CQ * q].x = mm_[q];
+      } else if (i == jn + 1) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (CQ * q <= jn + 1) rowb[nb][cp + CQ * q].y = mm_[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && t == 0) atomicOr(d_err, DEV_COLLAPSE);
+  if (i < m) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = cp + CQ * q;
+      if (k < m) Linv[i * ldl + k] = mm_[q];
+    }
+  }
+  __syncthreads();
+}
+
+static const int g_chol2 = tune_env("PPCA_CHOL2", 2);   // 0 one-step, 1 two-step, 2 two-step packed
 
 template <int CQ>
 __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
                                                            double* __restrict__ Linv, int* __restrict__ row_map,
-                                                           int* __restrict__ m_out, int* d_err, bool two_step) {
+                                                           int* __restrict__ m_out, int* d_err, int variant) {
   pdl_enter();
-  if (two_step) chol_inv_sweep2<CQ>(G, m, Linv, m, d_err);
+  if (variant == 2) chol_inv_sweep2p<CQ>(G, m, Linv, m, d_err);
+  else if (variant == 1) chol_inv_sweep2<CQ>(G, m, Linv, m, d_err);
   else chol_inv_sweep<CQ>(G, m, Linv, m, nullptr, d_err);
   if (threadIdx.x < m) row_map[threadIdx.x] = threadIdx.x;
   if (threadIdx.x == 0) *m_out = m;
