@@ -21,6 +21,8 @@ int g_pdl = tune_env("PPCA_PDL", 1);
 
 // ABI entry: select the device and order the library stream after the caller's stream
 static void enter(Ctx* c) {
+  c->wprep_for = nullptr;                       // a fused operand split never outlives the call that wrote it
+  c->s_skip = false;
   cudaSetDevice(c->device);
   if (c->own_stream) {
     cudaEventRecord(c->fork_ev, c->user_stream);
@@ -585,6 +587,8 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   c->side_busy = theta_hist_host != nullptr;
   // one GPU with the θ history: S only feeds the side-stream Ritz solve, so its reduction moves there too
   c->s_defer = theta_hist_host != nullptr && c->nccl_comm == nullptr;
+  // no θ history on one rank: S = YᵀY of the pass is not used at all (W comes from Z alone)
+  c->s_skip = theta_hist_host == nullptr && c->nccl_comm == nullptr;
   if (c->s_defer) {
     cudaEventCreateWithFlags(&c->s_ev_pass, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->s_ev_red, cudaEventDisableTiming);
@@ -669,6 +673,7 @@ ppca_status ppca_prime_power(ppca_ctx* h, const ppca_matrix* X, int m, int iters
   }
   c->prep_ev = nullptr;
   c->wprep_for = nullptr;
+  c->s_skip = false;
   c->side_busy = false;
   if (c->s_pending) pass_reduce_deferred_s(c, Sbuf, c->side);   // an aborted loop: drain (result unused)
   ppca_status st2 = finish(c, "ppca_prime_power");
@@ -741,8 +746,10 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
       c->zp_defer = eigengame && !c->nccl_comm;
       const ppca_status pst = pass_power(c, &Xw, &plan, W, m, Q, P);
       c->zp_defer = false;
+      c->wprep_for = nullptr;                       // adopted by the pass (or not wanted)
       PPCA_TRY(pst);
     } else {
+      c->wprep_for = nullptr;
       float* Y = (float*)scratch(c, S_Y, (size_t)std::max<int64_t>(1, rows) * m * sizeof(float));
       if (!Y) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
       c->last_impl = 1;
@@ -752,7 +759,27 @@ static ppca_status minibatch_common(Ctx* c, const ppca_matrix* X, int m, int bat
     }
     PPCA_TRY(allreduce_zs(c, Q, (size_t)m * d, P, (size_t)m * m));
     if (eigengame) {
-      PPCA_TRY(eigengame_update(c, Q, P, W, vel, m, d, alpha, mu));
+      // the next window pass's operand split written by the update kernel itself (m = padded m: no zero rows)
+      WPrep wp{};
+      static const bool eg_prep = tune_env("PPCA_EG_PREP", 1) != 0;
+      bool want = eg_prep && plan.impl == 2 && ((m + 15) & ~15) == m && X->dtype != PPCA_F32;
+      if (want) {
+        const size_t bytes = (size_t)2 * m * d * 2 + (size_t)m * d * 4 + 256;
+        uint8_t* b = (uint8_t*)scratch(c, S_TC1, bytes);   // prep_w's buffer; nothing else reads it until then
+        want = b != nullptr;
+        if (want) {
+          wp.Wb = reinterpret_cast<__nv_bfloat16*>(b);
+          wp.Wr = reinterpret_cast<float*>(b + (((size_t)2 * m * d * 2 + 255) & ~(size_t)255));
+          wp.lo_off = (int64_t)m * d;
+        }
+      }
+      bool done = false;
+      PPCA_TRY(eigengame_update(c, Q, P, W, vel, m, d, alpha, mu, want ? &wp : nullptr, &done));
+      if (done) {
+        c->wprep_for = W;
+        c->wprep_b = wp.Wb;
+        c->wprep_r = wp.Wr;
+      }
     } else {
       PPCA_TRY(pass_reduce_deferred_z(c, Q));
       PPCA_TRY(oja_update(c, Q, P, W, vel, m, d, alpha, mu));

@@ -40,6 +40,7 @@ struct Ctx {
   // Ritz solve): the pass records s_ev_pass and leaves the partials; pass_reduce_deferred_s reduces them on a
   // given stream and records s_ev_red, which the next fused pass waits for before rewriting the partials
   bool s_defer = false;
+  bool s_skip = false;                // power loop without θ history on one rank: the pass's S is not reduced
   bool s_pending = false;
   cudaEvent_t s_ev_pass = nullptr, s_ev_red = nullptr;
   const double* s_part = nullptr;

@@ -842,7 +842,8 @@ static ppca_status pass_fused_power(Ctx* c, const ppca_matrix* X, const __nv_bfl
   PPCA_LAUNCH_CHECK(c, "xwz_fused_kernel");
   kernel_timer_mark(c, 0);
   *launched = true;
-  if (c->s_defer) {                               // S is reduced later, on the stream that consumes it
+  if (c->s_skip) {                                // the caller does not use S (power priming without θ history)
+  } else if (c->s_defer) {                        // S is reduced later, on the stream that consumes it
     cudaEventRecord(c->s_ev_pass, c->stream);
     c->s_pending = true;
     c->s_part = Spart;
@@ -988,7 +989,8 @@ static ppca_status pass_pair_power(Ctx* c, const ppca_matrix* X, const __nv_bflo
   }
 #endif
   kernel_timer_mark(c, 0);
-  if (c->s_defer) {                               // S is reduced later, on the stream that consumes it
+  if (c->s_skip) {                                // the caller does not use S (power priming without θ history)
+  } else if (c->s_defer) {                        // S is reduced later, on the stream that consumes it
     cudaEventRecord(c->s_ev_pass, c->stream);
     c->s_pending = true;
     c->s_part = Spart;

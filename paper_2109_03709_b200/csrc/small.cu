@@ -832,6 +832,17 @@ static size_t chol_inv_smem(int m) {
 // DFMA, warp-broadcast), the next chunk's IN loaded into registers while the current one is consumed.
 // short d (fewer 32-column chunks than SMs, e.g. C3's d = 1024): one CTA per 32 columns × row blocks, C
 // staged per CTA (measured faster there than the chunk-sweeping kernel below: 8.1 vs 11.6 µs for m = 64)
+// element e of the next pass operand W' = [W_hi; W_lo] (lo rows at lo_off) and W_r = hi + lo from the fp32 value
+// o, exactly as prep_w_kernel splits it (RN conversions, residual in fp32)
+__device__ __forceinline__ void split_store(__nv_bfloat16* Wb, float* Wr, int64_t lo_off, int64_t e, float o) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(o);
+  const float hf = __bfloat162float(h);
+  const __nv_bfloat16 l = __float2bfloat16_rn(o - hf);
+  Wb[e] = h;
+  Wb[lo_off + e] = l;
+  Wr[e] = hf + __bfloat162float(l);
+}
+
 constexpr int AP_COLS = 32;
 __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restrict__ C, int ldc, int rows,
                                                          int m_in, const int* __restrict__ row_map,
@@ -874,14 +885,7 @@ __global__ void __launch_bounds__(256) apply_rows_kernel(const double* __restric
       const float o = (float)((a0 + a1) + (a2 + a3));
       const int64_t e = (int64_t)oi * d + x;
       OUT[e] = o;
-      if (Wb) {                                   // the next pass's operand, as prep_w_kernel splits it
-        const __nv_bfloat16 h = __float2bfloat16_rn(o);
-        const float hf = __bfloat162float(h);
-        const __nv_bfloat16 l = __float2bfloat16_rn(o - hf);
-        Wb[e] = h;
-        Wb[lo_off + e] = l;
-        Wr[e] = hf + __bfloat162float(l);
-      }
+      if (Wb) split_store(Wb, Wr, lo_off, e, o);  // the next pass's operand
     }
   }
 }
@@ -1528,7 +1532,8 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
                                                         int64_t d, double alpha, double mu,
                                                         double* __restrict__ rowpart, int* d_err,
                                                         const float* __restrict__ Zp, int64_t nrg, int64_t dpad,
-                                                        int mp) {
+                                                        int mp, __nv_bfloat16* __restrict__ Wb, float* __restrict__ Wr,
+                                                        int64_t lo_off) {
   pdl_enter();
   EG_STAMP(0);
   namespace cg = cooperative_groups;
@@ -1699,7 +1704,9 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
         if (j >= m) break;
         const double v = nrm[j] > 0.0 ? (double)wkeep[q] * nrm[j] : (double)wkeep[q];
         if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
-        V[(int64_t)j * d + x] = (float)v;
+        const int64_t e = (int64_t)j * d + x;
+        V[e] = (float)v;
+        if (Wb) split_store(Wb, Wr, lo_off, e, (float)v);
       }
   } else {
     for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
@@ -1707,11 +1714,14 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
       if (x < d)
         for (int j = warp; j < m; j += nw) {
           const int64_t e = (int64_t)j * d + x;
+          float vf = V[e];
           if (nrm[j] > 0.0) {
-            const double v = (double)V[e] * nrm[j];
+            const double v = (double)vf * nrm[j];
             if (!isfinite(v)) atomicOr(d_err, DEV_NONFINITE);
-            V[e] = (float)v;
+            vf = (float)v;
+            V[e] = vf;
           }
+          if (Wb) split_store(Wb, Wr, lo_off, e, vf);
         }
     }
   }
@@ -1719,7 +1729,7 @@ __global__ void __launch_bounds__(256) eg_update_kernel(const float* __restrict_
 }
 
 static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
-                                   double alpha, double mu, ppca_status* st) {
+                                   double alpha, double mu, ppca_status* st, const WPrep* prep) {
   *st = PPCA_OK;
   const int64_t nchunks = ceil_div(d, (int64_t)EG_XC);
   const size_t smem = ((size_t)m * m + 3 * (size_t)m) * sizeof(double) +
@@ -1763,7 +1773,8 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
     mp = c->zp_mp;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, eg_update_kernel, MV, A, V, vel, m, d, alpha, mu, rowpart, c->d_err, Zp,
-                                     nrg, dpad, mp);
+                                     nrg, dpad, mp, prep ? prep->Wb : nullptr, prep ? prep->Wr : nullptr,
+                                     prep ? prep->lo_off : (int64_t)0);
   if (e == cudaSuccess) c->zp_pending = false;
 #ifdef PPCA_EXPERIMENTS
   static const int eg_clk = tune_env("PPCA_EG_CLK", 0);
@@ -1785,12 +1796,16 @@ static bool eigengame_update_fused(Ctx* c, const float* MV, const double* A, flo
 }
 
 ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m, int64_t d,
-                             double alpha, double mu) {
+                             double alpha, double mu, const WPrep* prep, bool* prep_done) {
   static int multi = -1;                          // PPCA_EG_MULTI=1: the 5-launch sequence (comparison)
   if (multi < 0) multi = tune_env("PPCA_EG_MULTI", 0);
+  if (prep_done) *prep_done = false;
   if (!multi) {
     ppca_status st;
-    if (eigengame_update_fused(c, MV, A, V, vel, m, d, alpha, mu, &st)) return st;
+    if (eigengame_update_fused(c, MV, A, V, vel, m, d, alpha, mu, &st, prep)) {
+      if (prep_done) *prep_done = prep != nullptr && st == PPCA_OK;
+      return st;
+    }
   }
   PPCA_TRY(pass_reduce_deferred_z(c, const_cast<float*>(MV)));   // the multi-launch sequence reads Z itself
   double* Cf = (double*)scratch(c, S_SMALL, (size_t)m * m * sizeof(double) + (size_t)m * sizeof(double) + 64);

@@ -57,8 +57,9 @@ ppca_status oja_update(Ctx* c, const float* Q, const double* P, float* W, float*
 bool oja_persistent(Ctx* c, const ppca_matrix* X, int m, int batch, double alpha, double mu, int64_t s0,
                     int64_t steps, float* W, float* vel, ppca_status* st);
 // EigenGame update: coefficients from A, r = 2MV − 2 N·MV − 2U∘V, Nesterov, renormalise.
+// prep: also write the next window pass's operand split of V (prep_done: it was written — the fused kernel ran)
 ppca_status eigengame_update(Ctx* c, const float* MV, const double* A, float* V, float* vel, int m,
-                             int64_t d, double alpha, double mu);
+                             int64_t d, double alpha, double mu, const WPrep* prep = nullptr, bool* prep_done = nullptr);
 
 // dots[i] = <E_i, T_i> in fp64.
 // Prop. 3 checker (reading R28): from the stacked Gram G ([B; T], ld g) and S, the angles between π_S(t_i)
