@@ -200,35 +200,53 @@ __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __rest
   }
 }
 
-// Z[j][x] = Σ_g Zp[g][x][j] for a few row groups (the short windows of the minibatch steps, nrg ≤ 16): thread =
-// 4 consecutive features of one column (one float4 per partial, all nrg loads in flight), sums in g order in
-// fp64; a block covers 256·4/mp columns and leaves through shared memory as runs of Z's rows.
+// Z[j][x] = Σ_g Zp[g][x][j] for a few row groups (the short windows of the minibatch steps and C5's kernel B,
+// nrg ≤ 16): thread = 4 consecutive features of CPT columns (one float4 per partial and column, 16 loads in
+// flight: CPT = 4 for nrg ≤ 4), sums in g order in fp64; a block covers CPT·256·4/mp ≤ 64 columns and leaves
+// through shared memory as runs of Z's rows (C5, nrg = 4, mp = 128: 32-column blocks write whole 128-byte lines
+// of every feature row instead of 32-byte sectors; same sums, same bits).
+template <int CPT>
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z, int64_t ds) {
   pdl_enter();
   __shared__ float tr[128][65];
+  constexpr int GB = 16 / CPT;                       // partials per batch of loads
   const int tpc = mp >> 2;                           // threads per column (mp ≤ 128, multiple of 16)
-  const int cpb = 256 / tpc;                         // columns per block (≤ 64)
+  const int cpp = 256 / tpc;                         // columns per sweep of the block
+  const int cpb = cpp * CPT;                         // columns per block (≤ 64)
   const int64_t x0 = (int64_t)blockIdx.x * cpb;
   const int xl = threadIdx.x / tpc, j4 = (threadIdx.x % tpc) * 4;
-  const int64_t x = x0 + xl;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  if (x < d) {
-    const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
-    const int64_t gs = dpad * mp / 4;
-    for (int64_t g0 = 0; g0 < nrg; g0 += 16) {
-      float4 v[16];
+  double a[CPT][4];
 #pragma unroll
-      for (int gg = 0; gg < 16; ++gg)
-        if (g0 + gg < nrg) v[gg] = __ldg(src + (g0 + gg) * gs);
+  for (int cc = 0; cc < CPT; ++cc) a[cc][0] = a[cc][1] = a[cc][2] = a[cc][3] = 0.0;
+  const int64_t gs = dpad * mp / 4;
+  for (int64_t g0 = 0; g0 < nrg; g0 += GB) {
+    float4 v[CPT][GB];
 #pragma unroll
-      for (int gg = 0; gg < 16; ++gg)
-        if (g0 + gg < nrg) {
-          a0 += (double)v[gg].x; a1 += (double)v[gg].y; a2 += (double)v[gg].z; a3 += (double)v[gg].w;
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int64_t x = x0 + xl + cc * cpp;
+      const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
+#pragma unroll
+      for (int gg = 0; gg < GB; ++gg)
+        if (x < d && g0 + gg < nrg) v[cc][gg] = __ldg(src + (g0 + gg) * gs);
+    }
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int64_t x = x0 + xl + cc * cpp;
+#pragma unroll
+      for (int gg = 0; gg < GB; ++gg)
+        if (x < d && g0 + gg < nrg) {
+          a[cc][0] += (double)v[cc][gg].x; a[cc][1] += (double)v[cc][gg].y;
+          a[cc][2] += (double)v[cc][gg].z; a[cc][3] += (double)v[cc][gg].w;
         }
     }
   }
-  tr[j4][xl] = (float)a0; tr[j4 + 1][xl] = (float)a1; tr[j4 + 2][xl] = (float)a2; tr[j4 + 3][xl] = (float)a3;
+#pragma unroll
+  for (int cc = 0; cc < CPT; ++cc) {
+    const int c = xl + cc * cpp;
+    tr[j4][c] = (float)a[cc][0]; tr[j4 + 1][c] = (float)a[cc][1];
+    tr[j4 + 2][c] = (float)a[cc][2]; tr[j4 + 3][c] = (float)a[cc][3];
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < m * cpb; e += 256) {
     const int j = e / cpb, c = e % cpb;
@@ -341,8 +359,17 @@ static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad,
   if (nrg > 16)
     launch_pdl(reduce_zp_cols_kernel, dim3(dim3((unsigned)d, (unsigned)ceil_div(m, 32))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z,
                                                                                             ds);
-  else
-    launch_pdl(reduce_zp_kernel, dim3((unsigned)ceil_div(d, (int64_t)(256 / (mp / 4)))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+  else {
+    const int cpp = 256 / (mp / 4);                  // columns per block sweep; CPT sweeps per block, ≤ 64 columns
+    static const int cpt_cap = tune_env("PPCA_ZP_CPT", 4);
+    const int cpt = std::min(std::min(nrg <= 4 ? 4 : (nrg <= 8 ? 2 : 1), std::max(1, 64 / cpp)), cpt_cap);
+    if (cpt >= 4)
+      launch_pdl(reduce_zp_kernel<4>, dim3((unsigned)ceil_div(d, (int64_t)(4 * cpp))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+    else if (cpt >= 2)
+      launch_pdl(reduce_zp_kernel<2>, dim3((unsigned)ceil_div(d, (int64_t)(2 * cpp))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+    else
+      launch_pdl(reduce_zp_kernel<1>, dim3((unsigned)ceil_div(d, (int64_t)cpp)), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+  }
 }
 
 // ============================================================================ host side

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
                                                    double* __restrict__ gLinv, double* __restrict__ gT1,
                                                    double* __restrict__ theta, double* __restrict__ R, int* d_err) {
   const bool vectors = R != nullptr;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const int mm = (m + 1) & ~1;          // even (a dummy player for odd m)
   const int np = mm / 2;
   double* A = sm;                                     // mm × mm
@@ -191,9 +191,12 @@ __global__ void __launch_bounds__(512) ritz_kernel(const double* __restrict__ S,
 __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restrict__ S, const double* __restrict__ Bm,
                                                           int m, double* __restrict__ gLinv, double* __restrict__ gT1,
                                                           double* __restrict__ theta, int* d_err,
-                                                          double* __restrict__ R = nullptr, int top = 0) {
+                                                          double* __restrict__ R = nullptr, int top = 0,
+                                                          int opt = 0) {
   // top (1 ≤ top ≤ m): only the top largest eigenpairs are formed (the refine needs k of m); 0 = all
-  extern __shared__ double sm[];
+  // opt bit 0: Sturm counts by the division-free product recurrence; bit 1: warp-per-row matvec in the
+  // tridiagonalisation
+  extern __shared__ __align__(16) double sm[];
   if (top <= 0 || top > m) top = m;
   const int jlo = m - top;                            // ascending index of the smallest eigenpair formed
   const bool small = m <= 64;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   // 1. L = chol(B), L⁻¹, C = L⁻¹ S L⁻ᵀ (symmetrised)
   if (tid == 0) g_ritz_clk[0] = clock64();
   if (m <= 64 && nt == 512) {                        // register sweep (small.cu): Cholesky and L⁻¹ together
-    ppca::chol_inv_sweep<8>(Bm, m, Linv, m, keep, d_err);
+    ppca::chol_inv_sweep2t<2, 16>(Bm, m, Linv, m, d_err, m, keep);
     if (tid == 0) g_ritz_clk[1] = g_ritz_clk[2] = clock64();
   } else {
     ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return Bm[e]; }, [&](int64_t e, double v) { A[e] = v; });
@@ -222,6 +225,39 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   }
   ppca::copy_batched<16>(tid, m * m, nt, [&](int64_t e) { return S[e]; }, [&](int64_t e, double v) { A[e] = v; });
   __syncthreads();
+  if ((opt & 4) && m == 64 && nt == 512) {
+    // both triangular products on 2 × 4 register tiles: OUT[r][c] = Σ_{t ≤ r} L⁻¹[r][t]·B[t][c] with B's rows
+    // contiguous along c (16 column tiles per warp: conflict-free 16-byte loads) and two L⁻¹ scalars per t —
+    // 4 shared loads per 8 DFMA instead of 2 per 1 (the per-element loops below are bound by shared-memory
+    // bandwidth: 25 µs).  Product 1 is (L⁻¹S)ᵀ = S L⁻ᵀ, stored transposed.
+    const int tr = tid >> 4, tc = tid & 15, r0 = 2 * tr, c0 = 4 * tc;
+    for (int pass = 0; pass < 2; ++pass) {
+      const double* Bsrc = pass == 0 ? A : T1;
+      double acc[2][4] = {};
+      for (int t = 0; t <= r0 + 1; ++t) {
+        const double l0 = Linv[r0 * m + t], l1 = Linv[(r0 + 1) * m + t];   // L⁻¹[r0][r0+1] is an exact zero
+        const double2 b01 = *reinterpret_cast<const double2*>(Bsrc + t * m + c0);
+        const double2 b23 = *reinterpret_cast<const double2*>(Bsrc + t * m + c0 + 2);
+        acc[0][0] = fma(l0, b01.x, acc[0][0]);
+        acc[0][1] = fma(l0, b01.y, acc[0][1]);
+        acc[0][2] = fma(l0, b23.x, acc[0][2]);
+        acc[0][3] = fma(l0, b23.y, acc[0][3]);
+        acc[1][0] = fma(l1, b01.x, acc[1][0]);
+        acc[1][1] = fma(l1, b01.y, acc[1][1]);
+        acc[1][2] = fma(l1, b23.x, acc[1][2]);
+        acc[1][3] = fma(l1, b23.y, acc[1][3]);
+      }
+      __syncthreads();                                 // pass 1 overwrites A, which pass 0 read
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          if (pass == 0) T1[(c0 + v) * m + r0 + u] = acc[u][v];   // T1[i][j] = (L⁻¹S)[j][i]
+          else A[(r0 + u) * m + c0 + v] = acc[u][v];
+        }
+      __syncthreads();
+    }
+  } else {
   for (int e = tid; e < m * m; e += nt) {
     const int j = e / m, i = e % m;
     double s = 0.0;
@@ -236,6 +272,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
     A[e] = s;
   }
   __syncthreads();
+  }
   for (int e = tid; e < m * m; e += nt) {
     const int i = e / m, j = e % m;
     if (i < j) {
@@ -290,6 +327,35 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
       // p = β C' v, C' = A[k+1.., k+1..]: G threads per row (consecutive lanes), shuffle-reduced
       const int G = nt / n1 >= 4 ? 4 : (nt / n1 >= 2 ? 2 : 1);
       double vp = 0.0;
+      if (opt & 2) {
+        // a warp per row, lanes along it (consecutive addresses: no bank conflicts — G lanes per row put the
+        // rows of a warp m doubles apart, on the same banks), four rows' reductions interleaved
+        const int nw = nt >> 5;
+        for (int r0 = warp; r0 < n1; r0 += 4 * nw) {
+          double acc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = r0 + u * nw;
+            acc[u] = 0.0;
+            if (i < n1) {
+              const double* row = A + (k + 1 + i) * m + (k + 1);
+              for (int j = lane; j < n1; j += 32) acc[u] = fma(row[j], vec[j], acc[u]);
+            }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = r0 + u * nw;
+            if (i < n1 && lane == 0) {
+              pv[i] = beta * acc[u];
+              vp = fma(vec[i], beta * acc[u], vp);
+            }
+          }
+        }
+      } else
       for (int b0 = 0; b0 < n1; b0 += nt / G) {
         const int base = b0 + tid / G, q = tid % G;
         const bool act = base < n1;
@@ -304,7 +370,7 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
           vp = fma(vec[base], beta * acc, vp);
         }
       }
-      vp = ppca::warp_sum(vp);
+      if (!(opt & 2)) vp = ppca::warp_sum(vp);
       if (lane == 0) red_k[warp] = vp;
       __syncthreads();
       double kk = 0.0;
@@ -348,7 +414,18 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
   const int rounds = G == 8 ? 14 : (G == 4 ? 19 : (G == 2 ? 27 : 42));
   // squared off-diagonal once (bsq[i] = b_{i-1}², bsq[0] unused), so the count loop is load + rcp + two DFMA
   double* bsq = pv;                                   // (pv is free after the tridiagonalisation)
-  for (int i = tid; i < m; i += nt) bsq[i] = i > 0 ? tb[i - 1] * tb[i - 1] : 0.0;
+  double* tas = vec;                                  // a_i / span (vec is free too)
+  const double inv_span = 1.0 / span;
+  for (int i = tid; i < m; i += nt) {
+    const double bi = i > 0 ? tb[i - 1] : 0.0;
+    if (opt & 1) {
+      const double bs = bi * inv_span;
+      bsq[i] = bs * bs;
+      tas[i] = ta[i] * inv_span;
+    } else {
+      bsq[i] = bi * bi;
+    }
+  }
   __syncthreads();
   for (int b0 = jlo; b0 < m; b0 += nt / G) {            // uniform trip counts: every lane reaches the shuffles
     const int q = tid % G, j = b0 + tid / G;
@@ -358,14 +435,40 @@ __global__ void __launch_bounds__(512) ritz_values_kernel(const double* __restri
     for (int round = 0; round < rounds; ++round) {
       const double x = L + (U - L) * (double)(q + 1) / (double)(G + 1);
       int cnt = 0;
-      double dd = ta[0] - x;
-      if (dd == 0.0) dd = -1e-300;
-      cnt += dd < 0.0;
-#pragma unroll 4
-      for (int i = 1; i < mm; ++i) {                   // (reciprocal instead of an IEEE division: only signs count)
-        dd = (ta[i] - x) - bsq[i] * __drcp_rn(dd);
+      if (opt & 1) {
+        // Sturm count without the reciprocal: q_{i+1} = (a_i − x)·q_i − b_{i−1}²·q_{i−1} (q_0 = 1), the leading
+        // principal minors of T − xI, d_i = q_{i+1}/q_i; count = sign changes along q.  One dependent DFMA per
+        // row instead of reciprocal + DFMA.  T is scaled by 1/span (|a − x| ≤ 1, b² ≤ 1: growth ≤ 2 per row, no
+        // overflow in 128 rows); the pair is rescaled by a power of two every second row against underflow; an
+        // exact zero takes the sign opposite to its predecessor (the d_i = −tiny rule of the quotient form).
+        const double xs = x * inv_span;
+        double qp = 1.0, qc = tas[0] - xs;
+        if (qc == 0.0) qc = -1e-280;
+        cnt += qc < 0.0;
+#pragma unroll 2
+        for (int i = 1; i < mm; ++i) {
+          double qn = fma(tas[i] - xs, qc, -(bsq[i] * qp));
+          if (qn == 0.0) qn = -copysign(1e-280, qc);
+          cnt += ((__double2hiint(qn) ^ __double2hiint(qc)) >> 31) & 1;
+          qp = qc;
+          qc = qn;
+          if (i & 1) {                                 // 2^−e, e the exponent of max(|q_i|, |q_{i+1}|)
+            const int eh = __double2hiint(fmax(fabs(qc), fabs(qp))) & 0x7ff00000;
+            const double sc = __hiloint2double(0x7fe00000 - eh, 0);
+            qc *= sc;
+            qp *= sc;
+          }
+        }
+      } else {
+        double dd = ta[0] - x;
         if (dd == 0.0) dd = -1e-300;
         cnt += dd < 0.0;
+#pragma unroll 4
+        for (int i = 1; i < mm; ++i) {                 // (reciprocal instead of an IEEE division: only signs count)
+          dd = (ta[i] - x) - bsq[i] * __drcp_rn(dd);
+          if (dd == 0.0) dd = -1e-300;
+          cnt += dd < 0.0;
+        }
       }
       if (!act) cnt = 0;
       // the G probes split [L, U] into G+1 parts: keep the part holding the (j+1)-th eigenvalue

@@ -245,8 +245,13 @@ static void vec_gram_split(const Ctx* c, int m, int64_t d, int* nsplit_out, int6
     const int64_t ns = std::max<int64_t>(1, std::min(want, ceil_div(d, (int64_t)64)));
     cps = ceil_div(ceil_div(d, ns), (int64_t)64) * 64;
   } else {
+    // m > 120 (vec_gram_bal16_kernel: 128 threads, 255 registers, 34 KB): two slabs per SM, so that two CTAs are
+    // co-resident and every sub-partition has two warps to issue DFMAs from (one warp leaves the fp64 pipe idle
+    // between its loads)
+    static const int per_sm16 = tune_env("PPCA_GRAM_CPSM", 2);
     const int64_t stages = ceil_div(d, (int64_t)GK);
-    cps = ceil_div(stages, std::min<int64_t>(stages, (int64_t)c->sm_count)) * GK;
+    const int64_t slabs = (int64_t)c->sm_count * (ceil_div(m, 8) >= 16 ? per_sm16 : 1);
+    cps = ceil_div(stages, std::min<int64_t>(stages, slabs)) * GK;
   }
   *nsplit_out = (int)ceil_div(d, cps);
   *cps_out = cps;
@@ -718,7 +723,149 @@ __device__ void chol_inv_sweep2p(const double* __restrict__ G, int m, double* __
   __syncthreads();
 }
 
-static const int g_chol2 = tune_env("PPCA_CHOL2", 2);   // 0 one-step, 1 two-step, 2 two-step packed
+// The packed two-step sweep on register tiles: thread = RI consecutive rows × the columns ≡ cp (mod CQ) of A and of
+// M ((64/RI)·CQ threads; threads beyond that only take part in the barriers).  chol_inv_sweep2p delivers
+// 64·64·2·16 B = 128 KB of published operands to registers per step whatever its CQ (every element loads its own
+// column's double2: ≈ 1000 cycles of the 128 B/clk shared-memory pipe — the measured 0.9 µs per step); a thread
+// that owns RI rows loads each column operand once for all of them: (2·64/CQ + RI + 2) 16-byte loads per thread,
+// 56 KB per step for RI = 4, CQ = 16.  Threads whose rows are all finished (< j) skip the step's arithmetic and
+// loads.  Every element sees the operations of chol_inv_sweep2p in the same order: bitwise the same L⁻¹.
+template <int RI, int CQ>
+__device__ void chol_inv_sweep2t(const double* __restrict__ G, int m, double* __restrict__ Linv, int ldl, int* d_err,
+                                 int ldg = -1, int* __restrict__ keep = nullptr) {
+  static_assert(CQ >= 2 && RI >= 2 && RI % 2 == 0 && CF_M % RI == 0 && CF_M % CQ == 0, "tile shape");
+  if (ldg < 0) ldg = m;
+  __shared__ double2 colb[2][CF_M];
+  __shared__ double2 rowb[2][CF_M];
+  constexpr int NQ = CF_M / CQ;
+  constexpr int NT = (CF_M / RI) * CQ;
+  const int t = threadIdx.x, ig = t / CQ, cp = t % CQ, i0 = ig * RI;
+  const bool act = t < NT;
+  double a[RI][NQ], mm_[RI][NQ];
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < RI; ++r)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = i0 + r, k = cp + CQ * q;
+        a[r][q] = (i < m && k < m) ? G[i * ldg + k] : (i == k ? 1.0 : 0.0);
+        mm_[r][q] = i == k ? 1.0 : 0.0;
+      }
+    if (cp == 0) {
+#pragma unroll
+      for (int r = 0; r < RI; ++r) colb[0][i0 + r].x = a[r][0];
+    }
+    if (cp == 1) {
+#pragma unroll
+      for (int r = 0; r < RI; ++r) colb[0][i0 + r].y = a[r][0];
+    }
+    if (ig == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) rowb[0][cp + CQ * q] = make_double2(mm_[0][q], mm_[1][q]);
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < CF_M; j += 2) {
+    const int b = (j >> 1) & 1;
+    if (act && i0 + RI - 1 >= j) {                   // rows < j are finished in A and in M
+      const double p0 = colb[b][j].x;
+      const double2 cj1 = colb[b][j + 1];
+      const double c0j1 = cj1.x, c1j1 = cj1.y;
+      const bool ok0 = p0 > 0.0 && isfinite(p0);
+      const double r0 = ok0 ? rsqrt(p0) : 0.0;
+      const double g0 = r0 * r0;
+      const double h = c0j1 * g0;
+      const double p1 = fma(-h, c0j1, c1j1);
+      const bool ok1 = p1 > 0.0 && isfinite(p1);
+      const double r1 = ok1 ? rsqrt(p1) : 0.0;
+      const double g1 = r1 * r1;
+      bad |= !ok0 || !ok1;
+      double F0[RI], F1[RI], fa0[RI], fa1[RI];
+#pragma unroll
+      for (int r = 0; r < RI; ++r) {
+        const int i = i0 + r;
+        const double2 ci = colb[b][i];
+        const double f0 = ci.x * g0;
+        const double c1pi = fma(-f0, c0j1, ci.y);
+        const bool live = i > j + 1;
+        F0[r] = i == j ? 1.0 - r0 : f0;
+        F1[r] = i == j + 1 ? 1.0 - r1 : (live ? c1pi * g1 : 0.0);
+        fa0[r] = live ? f0 : 0.0;
+        fa1[r] = live ? c1pi * g1 : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int kk = cp + CQ * q;
+        if (CQ * q + CQ - 1 >= j + 2) {
+          const double2 ck = colb[b][kk];
+          const double c1k = fma(-(ck.x * g0), c0j1, ck.y);
+#pragma unroll
+          for (int r = 0; r < RI; ++r) {
+            a[r][q] = fma(-fa0[r], ck.x, a[r][q]);
+            a[r][q] = fma(-fa1[r], c1k, a[r][q]);
+          }
+        }
+        if (CQ * q <= j + 1) {
+          const double2 mk = rowb[b][kk];
+          const double mj1 = fma(-h, mk.x, mk.y);
+#pragma unroll
+          for (int r = 0; r < RI; ++r) {
+            mm_[r][q] = fma(-F0[r], mk.x, mm_[r][q]);
+            mm_[r][q] = fma(-F1[r], mj1, mm_[r][q]);
+          }
+        }
+      }
+      if (j + 2 < CF_M) {                            // publish columns j+2, j+3 of A and rows j+2, j+3 of M
+        const int jn = j + 2, nb = b ^ 1;
+        if (cp == jn % CQ) {
+#pragma unroll
+          for (int r = 0; r < RI; ++r) colb[nb][i0 + r].x = i0 + r >= jn ? a[r][jn / CQ] : 0.0;
+        }
+        if (cp == (jn + 1) % CQ) {
+#pragma unroll
+          for (int r = 0; r < RI; ++r) colb[nb][i0 + r].y = i0 + r >= jn ? a[r][(jn + 1) / CQ] : 0.0;
+        }
+        if (ig == jn / RI) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            if (CQ * q <= jn + 1) rowb[nb][cp + CQ * q] = make_double2(mm_[jn % RI][q], mm_[jn % RI + 1][q]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad) && t == 0) atomicOr(d_err, DEV_COLLAPSE);
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < RI; ++r)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = i0 + r, k = cp + CQ * q;
+        if (i < m && k < m) Linv[i * ldl + k] = mm_[r][q];
+      }
+  }
+  if (keep && t < m) keep[t] = 1;
+  __syncthreads();
+}
+
+template <int RI, int CQ>
+__global__ void __launch_bounds__((CF_M / RI) * CQ) chol_inv_regt_kernel(const double* __restrict__ G, int m,
+                                                                      double* __restrict__ Linv,
+                                                                      int* __restrict__ row_map,
+                                                                      int* __restrict__ m_out, int* d_err) {
+  pdl_enter();
+  chol_inv_sweep2t<RI, CQ>(G, m, Linv, m, d_err);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) row_map[i] = i;
+  if (threadIdx.x == 0) *m_out = m;
+}
+
+// 0 one-step, 1 two-step, 2 two-step packed, 3–6 packed on register tiles of (2, 4), (4, 4), (4, 8), (2, 8) rows ×
+// columns per thread.  Same box, C3 chain (profiles/r2_s6_chol_tiles_ab.txt): 2: 35.5 µs, 3: 26.5 µs, 4: 37.5 µs,
+// 5: 47 µs, 6: 35 µs from the Gram's split sum to the sweep's end — the sweep needs the 512 threads (latency), and
+// two rows per thread take a third off its shared-memory loads
+static const int g_chol2 = tune_env("PPCA_CHOL2", 3);
 
 template <int CQ>
 __global__ void __launch_bounds__(64 * CQ) chol_inv_reg_kernel(const double* __restrict__ G, int m,
@@ -770,7 +917,7 @@ __global__ void __launch_bounds__(512) chol_inv_blk_kernel(const double* __restr
   double* A22 = L21 + BK64 * BKL;                   // A22', then T = L21·L11⁻¹
   double* L22i = A22 + BK64 * BKL;                  // L22⁻¹
   const int m2 = m - BK64;
-  chol_inv_sweep<8>(G, BK64, L11i, BKL, nullptr, d_err, m);
+  chol_inv_sweep2t<2, 16>(G, BK64, L11i, BKL, d_err, m);
   for (int e = threadIdx.x; e < BK64 * BK64; e += 512) {            // A21 (rows ≥ m2 zero)
     const int i = e / BK64, k = e % BK64;
     A22[i * BKL + k] = i < m2 ? G[(BK64 + i) * m + k] : 0.0;
@@ -783,7 +930,7 @@ __global__ void __launch_bounds__(512) chol_inv_blk_kernel(const double* __restr
   }
   __syncthreads();
   mm64(L21, false, L21, true, A22, -1.0, L22i, BKL);             // A22' = A22 − L21·L21ᵀ
-  chol_inv_sweep<8>(A22, m2, L22i, BKL, nullptr, d_err, BKL);
+  chol_inv_sweep2t<2, 16>(A22, m2, L22i, BKL, d_err, BKL);
   mm64(L21, false, L11i, false, A22, 1.0, nullptr, 0);           // T = L21·L11⁻¹
   mm64(L22i, false, A22, false, L21, -1.0, nullptr, 0);          // X21 = −L22⁻¹·T
   for (int e = threadIdx.x; e < m * m; e += 512) {
@@ -808,6 +955,22 @@ static void launch_chol_inv_reg(const double* G, int m, double* Linv, int* row_m
     if (first_on_device(&attr, dev))
       cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(chol_inv_blk_kernel, dim3(1), dim3(512), smem, st, G, m, Linv, row_map, m_out, d_err);
+    return;
+  }
+  if (g_chol2 == 3) {        // register tiles: 2 rows × 4 columns, 512 threads
+    launch_pdl(chol_inv_regt_kernel<2, 16>, dim3(1), dim3(512), 0, st, G, m, Linv, row_map, m_out, d_err);
+    return;
+  }
+  if (g_chol2 == 4) {        // 4 rows × 4 columns, 256 threads
+    launch_pdl(chol_inv_regt_kernel<4, 16>, dim3(1), dim3(256), 0, st, G, m, Linv, row_map, m_out, d_err);
+    return;
+  }
+  if (g_chol2 == 5) {        // 4 rows × 8 columns, 128 threads
+    launch_pdl(chol_inv_regt_kernel<4, 8>, dim3(1), dim3(128), 0, st, G, m, Linv, row_map, m_out, d_err);
+    return;
+  }
+  if (g_chol2 == 6) {        // 2 rows × 8 columns, 256 threads
+    launch_pdl(chol_inv_regt_kernel<2, 8>, dim3(1), dim3(256), 0, st, G, m, Linv, row_map, m_out, d_err);
     return;
   }
   if (g_chol_cq == 4)
@@ -1145,6 +1308,7 @@ ppca_status ritz_debug_clocks(unsigned long long* out8) {
   return PPCA_OK;
 }
 
+static const int g_ritz_opt = tune_env("PPCA_RITZ_OPT", 5);   // ritz_values_kernel's opt bits (ritz.cuh)
 ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double* theta_dev, double* R_dev,
                        cudaStream_t stream, int top) {
   double* scr = (double*)scratch(c, S_EVAL, (size_t)2 * m * m * sizeof(double));
@@ -1163,7 +1327,7 @@ ppca_status ritz_solve(Ctx* c, const double* S, const double* Bm, int m, double*
     }
     const size_t vsm = (R_dev && m <= 64) ? ritz::vectors_smem_bytes(m) : ritz::values_smem_bytes(m);
     ritz::ritz_values_kernel<<<1, 512, vsm, stream>>>(S, Bm, m, scr, scr + (size_t)m * m, theta_dev, c->d_err, R_dev,
-                                                      R_dev ? top : 0);
+                                                      R_dev ? top : 0, g_ritz_opt);
     PPCA_LAUNCH_CHECK(c, "ritz_values_kernel");
     return PPCA_OK;
   }
