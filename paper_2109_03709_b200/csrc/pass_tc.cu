@@ -205,11 +205,18 @@ __global__ void __launch_bounds__(256) reduce_zp_cols_kernel(const float* __rest
 // flight: CPT = 4 for nrg ≤ 4), sums in g order in fp64; a block covers CPT·256·4/mp ≤ 64 columns and leaves
 // through shared memory as runs of Z's rows (C5, nrg = 4, mp = 128: 32-column blocks write whole 128-byte lines
 // of every feature row instead of 32-byte sectors; same sums, same bits).
+// The partial loads go through cp.async into a per-thread staging slot ([slot][thread] float4: conflict-free), one
+// wait for all 16: in flight together by construction.  Register loads did not stay that way — with the loads under
+// the predicate of their use, and also with unconditional loads, ptxas places every conversion right behind its load
+// to save registers (SASS: LDG, 4 × F2F, LDG, …; a barrier between loads and sums did not hold them either), so the
+// 16 loads ran one DRAM latency after the other: 100 µs for C5's 134 MB of partials (ncu: long-scoreboard stalls,
+// 1.3 TB/s).
 template <int CPT>
 __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict__ Zp, int64_t nrg, int64_t dpad, int mp,
                                                         int m, int64_t d, float* __restrict__ Z, int64_t ds) {
   pdl_enter();
   __shared__ float tr[128][65];
+  extern __shared__ __align__(16) float4 stage[];    // [16][256]
   constexpr int GB = 16 / CPT;                       // partials per batch of loads
   const int tpc = mp >> 2;                           // threads per column (mp ≤ 128, multiple of 16)
   const int cpp = 256 / tpc;                         // columns per sweep of the block
@@ -220,24 +227,30 @@ __global__ void __launch_bounds__(256) reduce_zp_kernel(const float* __restrict_
 #pragma unroll
   for (int cc = 0; cc < CPT; ++cc) a[cc][0] = a[cc][1] = a[cc][2] = a[cc][3] = 0.0;
   const int64_t gs = dpad * mp / 4;
+  const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(stage + threadIdx.x);
   for (int64_t g0 = 0; g0 < nrg; g0 += GB) {
-    float4 v[CPT][GB];
+    if (g0 > 0) __syncwarp();                        // (own slots only: no block barrier between batches)
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
-      const int64_t x = x0 + xl + cc * cpp;
+      const int64_t x = min(x0 + xl + cc * cpp, d - 1);
       const float4* src = reinterpret_cast<const float4*>(Zp + x * mp + j4);
 #pragma unroll
       for (int gg = 0; gg < GB; ++gg)
-        if (x < d && g0 + gg < nrg) v[cc][gg] = __ldg(src + (g0 + gg) * gs);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st0 + (uint32_t)((cc * GB + gg) * 256 * 16)),
+                     "l"(src + min(g0 + gg, nrg - 1) * gs)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
       const int64_t x = x0 + xl + cc * cpp;
 #pragma unroll
       for (int gg = 0; gg < GB; ++gg)
         if (x < d && g0 + gg < nrg) {
-          a[cc][0] += (double)v[cc][gg].x; a[cc][1] += (double)v[cc][gg].y;
-          a[cc][2] += (double)v[cc][gg].z; a[cc][3] += (double)v[cc][gg].w;
+          const float4 v = stage[(cc * GB + gg) * 256 + threadIdx.x];
+          a[cc][0] += (double)v.x; a[cc][1] += (double)v.y;
+          a[cc][2] += (double)v.z; a[cc][3] += (double)v.w;
         }
     }
   }
@@ -363,12 +376,19 @@ static void launch_reduce_zp(Ctx* c, const float* Zp, int64_t nrg, int64_t dpad,
     const int cpp = 256 / (mp / 4);                  // columns per block sweep; CPT sweeps per block, ≤ 64 columns
     static const int cpt_cap = tune_env("PPCA_ZP_CPT", 4);
     const int cpt = std::min(std::min(nrg <= 4 ? 4 : (nrg <= 8 ? 2 : 1), std::max(1, 64 / cpp)), cpt_cap);
+    const size_t stage = (size_t)16 * 256 * sizeof(float4);   // 64 KB + 33 KB static: two CTAs per SM
+    static uint64_t attr = 0;
+    if (first_on_device(&attr, c->device)) {
+      cudaFuncSetAttribute(reduce_zp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+      cudaFuncSetAttribute(reduce_zp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+      cudaFuncSetAttribute(reduce_zp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+    }
     if (cpt >= 4)
-      launch_pdl(reduce_zp_kernel<4>, dim3((unsigned)ceil_div(d, (int64_t)(4 * cpp))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+      launch_pdl(reduce_zp_kernel<4>, dim3((unsigned)ceil_div(d, (int64_t)(4 * cpp))), dim3(256), stage, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
     else if (cpt >= 2)
-      launch_pdl(reduce_zp_kernel<2>, dim3((unsigned)ceil_div(d, (int64_t)(2 * cpp))), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+      launch_pdl(reduce_zp_kernel<2>, dim3((unsigned)ceil_div(d, (int64_t)(2 * cpp))), dim3(256), stage, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
     else
-      launch_pdl(reduce_zp_kernel<1>, dim3((unsigned)ceil_div(d, (int64_t)cpp)), dim3(256), 0, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
+      launch_pdl(reduce_zp_kernel<1>, dim3((unsigned)ceil_div(d, (int64_t)cpp)), dim3(256), stage, c->stream, Zp, nrg, dpad, mp, m, d, Z, ds);
   }
 }
 

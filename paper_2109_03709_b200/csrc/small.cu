@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(GRAM_MAXT) vec_gram_tiled_kernel(const float* 
 __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __restrict__ V, int m, int64_t d,
                                                        int64_t cols_per_split, double* __restrict__ P) {
   pdl_enter();
-  __shared__ float Vi[32][65];
-  __shared__ float Vj[32][65];
+  __shared__ double Vi[32][65];                      // staged as fp64: one conversion per staged value, not five
+  __shared__ double Vj[32][65];                      // per four DFMAs in the product loop (conversions issue at 1/4 rate)
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int64_t xb = (int64_t)blockIdx.z * cols_per_split;
   const int64_t xe = min(d, xb + cols_per_split);
@@ -119,16 +119,16 @@ __global__ void __launch_bounds__(256) vec_gram_generic_kernel(const float* __re
       for (int u = 0; u < 8; ++u) {
         const int e = threadIdx.x + 256 * u, r = e / 64, cidx = e % 64;
         const bool xin = x0 + cidx < xe;
-        Vi[r][cidx] = (i0 + r < m && xin) ? vi[u] : 0.f;
-        Vj[r][cidx] = (j0 + r < m && xin) ? vj[u] : 0.f;
+        Vi[r][cidx] = (i0 + r < m && xin) ? (double)vi[u] : 0.0;
+        Vj[r][cidx] = (j0 + r < m && xin) ? (double)vj[u] : 0.0;
       }
     }
     __syncthreads();
 #pragma unroll 8
     for (int cidx = 0; cidx < 64; ++cidx) {
-      double b = (double)Vj[tx][cidx];
+      const double b = Vj[tx][cidx];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) acc[a] = fma((double)Vi[ty * 4 + a][cidx], b, acc[a]);
+      for (int a = 0; a < 4; ++a) acc[a] = fma(Vi[ty * 4 + a][cidx], b, acc[a]);
     }
     __syncthreads();
   }
@@ -160,6 +160,12 @@ __global__ void __launch_bounds__(128) vec_gram_bal16_kernel(const float* __rest
   } else {
     bi = bj = t - 120;                             // diagonal tiles 0..7
   }
+  // The 8 threads of a quarter warp mostly hold one bi and 8 consecutive bj: their 16-byte loads of tile bj's
+  // columns are 64 bytes apart — two bank groups for 8 threads, a 4-way conflict on every b load (ncu: shared
+  // wavefronts 69 % of peak, fp64 pipe 28 %).  Thread bj starts its four loads at column pair bj/2 (mod 4), so even
+  // and odd bj each cover the four pairs: conflict-free; the accumulator columns are permuted the same way and
+  // un-permuted at the store.
+  const int rot = (bj >> 1) & 3;
   const int xt = 8 + (t >> 4), xs = t & 15;        // extra: diagonal tile 8..15, 2×2 sub-tile xs
   const int xr = xt * 8 + 2 * (xs >> 2), xc = xt * 8 + 2 * (xs & 3);
   double acc[8][8], ex[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(128) vec_gram_bal16_kernel(const float* __rest
       double a[8], b[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double2 va = pa[q], vb = pb[q];
+        const double2 va = pa[q], vb = pb[(q + rot) & 3];   // b[2q], b[2q+1] = columns 2·((q+rot)&3), +1 of tile bj
         a[2 * q] = va.x; a[2 * q + 1] = va.y;
         b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
       }
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(128) vec_gram_bal16_kernel(const float* __rest
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int gi = bi * 8 + i, gj = bj * 8 + j;
+      const int gi = bi * 8 + i, gj = bj * 8 + 2 * (((j >> 1) + rot) & 3) + (j & 1);
       if (gi < m && gj < m) {
         Pz[(int64_t)gi * m + gj] = acc[i][j];
         Pz[(int64_t)gj * m + gi] = acc[i][j];
@@ -1085,8 +1091,12 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
   pdl_enter();
   constexpr int RP = 32 * RPT, LDT = RP + 2;      // Cᵀ rows padded: 16-byte aligned, 4-way worst transposed store
   constexpr int PER = (128 * AT_COLS) / 256;      // staged IN values per thread (m_in ≤ 128)
-  extern __shared__ __align__(16) double ct[];    // [m_in][LDT] fp64, then [m_in][AT_COLS] fp32
-  float* ins = reinterpret_cast<float*>(ct + (size_t)m_in * LDT);
+  // [m_in][LDT] fp64, then IN staged as fp64 [m_in][2][8] double2 — (column pair p, column group cg): the
+  // conversion runs once per staged value (16 per thread and chunk) instead of four per thread and j (fp32 → fp64
+  // conversions issue at a quarter of the DFMA rate: as many pipe cycles as the 16 DFMAs they fed), and a quarter
+  // warp's 16-byte loads of one pair are 128 contiguous bytes
+  extern __shared__ __align__(16) double ct[];
+  double* ins = ct + (size_t)m_in * LDT;
   copy_batched<8>(threadIdx.x, (int64_t)rows * m_in, 256,
                   [&](int64_t e) {
                     const int i = (int)(e / m_in), j = (int)(e % m_in);
@@ -1124,7 +1134,8 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int e = threadIdx.x + 256 * u;
-      if (e < m_in * AT_COLS) ins[e] = nxt[u];
+      const int cc = e % AT_COLS;
+      if (e < m_in * AT_COLS) ins[(e / AT_COLS) * AT_COLS + ((cc & 3) >> 1) * 16 + (cc >> 2) * 2 + (cc & 1)] = (double)nxt[u];
     }
     __syncthreads();
     if (ch + gridDim.x < nchunks) fetch(ch + gridDim.x);
@@ -1135,7 +1146,8 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
       for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
 #pragma unroll 4
     for (int j = 0; j < jsplit; ++j) {
-      const float4 b = *reinterpret_cast<const float4*>(ins + j * AT_COLS + cg * 4);
+      const double2 b01 = *reinterpret_cast<const double2*>(ins + j * AT_COLS + cg * 2);
+      const double2 b23 = *reinterpret_cast<const double2*>(ins + j * AT_COLS + 16 + cg * 2);
       double a[RPT];
       if constexpr (RPT == 1) {
         a[0] = ct[j * LDT + i0];
@@ -1147,7 +1159,7 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
           a[r + 1] = v.y;
         }
       }
-      const double bb[4] = {(double)b.x, (double)b.y, (double)b.z, (double)b.w};
+      const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
       for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -1156,9 +1168,10 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
     if constexpr (RPT == 4) {
 #pragma unroll 4
       for (int j = jsplit; j < jend; ++j) {          // balanced lower: the high rows only
-        const float4 b = *reinterpret_cast<const float4*>(ins + j * AT_COLS + cg * 4);
+        const double2 b01 = *reinterpret_cast<const double2*>(ins + j * AT_COLS + cg * 2);
+        const double2 b23 = *reinterpret_cast<const double2*>(ins + j * AT_COLS + 16 + cg * 2);
         const double2 v = *reinterpret_cast<const double2*>(ct + j * LDT + rows_t[2]);
-        const double bb[4] = {(double)b.x, (double)b.y, (double)b.z, (double)b.w};
+        const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           acc[2][q] = fma(v.x, bb[q], acc[2][q]);
@@ -1184,7 +1197,7 @@ __global__ void __launch_bounds__(256) apply_tiled_kernel(const double* __restri
 template <int RPT>
 static void launch_apply_tiled(Ctx* c, const double* C, int ldc, int rows, int m_in, const int* row_map, bool lower,
                                const float* IN, int64_t d, float* OUT, cudaStream_t st) {
-  const size_t smem = (size_t)m_in * (32 * RPT + 2) * sizeof(double) + (size_t)m_in * AT_COLS * sizeof(float);
+  const size_t smem = (size_t)m_in * (32 * RPT + 2) * sizeof(double) + (size_t)m_in * AT_COLS * sizeof(double);
   static uint64_t attr = 0;
   if (first_on_device(&attr, c->device))
     cudaFuncSetAttribute(apply_tiled_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -35,6 +35,14 @@ if name in ("C2", "C4"):                         # minibatch priming steps (Oja 
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         fn(ctx, Xm, w.m, w.batch, w.alpha, w.momentum, iters, 0, W, vel, st)
         torch.cuda.synchronize()
+elif len(sys.argv) > 4 and sys.argv[4] == "refine":    # python tools/timeline.py C3 4 0 refine: one refine after `iters` steps
+    E = torch.empty((w.k, s.d), device="cuda")
+    P.ppca_prime_power(ctx, Xm, w.m, iters, w.init_seed, W)
+    P.ppca_refine_ex(ctx, Xm, W, w.m, w.k, E, flags=1)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        P.ppca_refine_ex(ctx, Xm, W, w.m, w.k, E, flags=1)
+        torch.cuda.synchronize()
 else:
     P.ppca_prime_power(ctx, Xm, w.m, 2, w.init_seed, W, theta_hist=hist)
     torch.cuda.synchronize()
