@@ -293,25 +293,36 @@ __global__ void __launch_bounds__(256) reduce_zp_gram_kernel(const float* __rest
 #pragma unroll
   for (int xi = 0; xi < ZG_X; ++xi) base[xi] = Zp + min(x0 + xi, d - 1) * mp;
   const int64_t gstride = dpad * mp;
+  // a batch's ZG_B·ZG_X·2 loads go through cp.async into the thread's own staging slots, one wait per batch: in
+  // flight together by construction (as register loads ptxas kept runs of four and put the conversions of each run
+  // behind it: four L2 round trips per batch instead of one)
+  __shared__ float stg[ZG_B * ZG_X * 2][256];
+  const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(&stg[0][threadIdx.x]);
+  const int jc0 = min(j0, m - 1), jc1 = min(j1, m - 1);
   for (int64_t g0 = warp; g0 < nrg; g0 += 8 * ZG_B) {
-    float v[ZG_B][ZG_X][2];
 #pragma unroll
     for (int u = 0; u < ZG_B; ++u) {
       const int64_t g = g0 + 8 * u;
 #pragma unroll
       for (int xi = 0; xi < ZG_X; ++xi) {
         const float* src = base[xi] + min(g, nrg - 1) * gstride;
-        v[u][xi][0] = j0 < m ? src[j0] : 0.f;
-        v[u][xi][1] = j1 < m ? src[j1] : 0.f;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(st0 + (uint32_t)(((u * ZG_X + xi) * 2) * 1024)),
+                     "l"(src + jc0)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(st0 + (uint32_t)(((u * ZG_X + xi) * 2 + 1) * 1024)),
+                     "l"(src + jc1)
+                     : "memory");
       }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int u = 0; u < ZG_B; ++u)
       if (g0 + 8 * u < nrg) {
 #pragma unroll
         for (int xi = 0; xi < ZG_X; ++xi) {
-          acc[xi][0] += (double)v[u][xi][0];
-          acc[xi][1] += (double)v[u][xi][1];
+          acc[xi][0] += (double)(j0 < m ? stg[(u * ZG_X + xi) * 2][threadIdx.x] : 0.f);
+          acc[xi][1] += (double)(j1 < m ? stg[(u * ZG_X + xi) * 2 + 1][threadIdx.x] : 0.f);
         }
       }
   }
@@ -634,35 +645,58 @@ static ppca_status run_ka(Ctx* c, const ppca_matrix* X, const __nv_bfloat16* Wb,
 // the block's rows also give a partial S_b = Σ_rows y yᵀ (fp64 products and sums, 4×4 register tiles per
 // thread) that launch_reduce_splits_f64 sums in block order.
 constexpr int YS_RB = 32;
+static size_t ysum_s_smem(int mp) {
+  const size_t rows = (size_t)YS_RB * (mp + 1);
+  return ((rows + 3) & ~(size_t)3) * sizeof(float) + (size_t)16 * 256 * sizeof(float) + rows * sizeof(double);
+}
+
 __global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Ypart, int ksplit, int64_t n, int mp,
                                                      int m, __nv_bfloat16* __restrict__ YT, int64_t ldyt,
                                                      double* __restrict__ Spart) {
   pdl_enter();
-  extern __shared__ float ysm[];                      // YS_RB × (mp + 1)
+  // YS_RB × (mp + 1) floats (the Y rows), [16][256] floats of load staging, YS_RB × (mp + 1) doubles (the same
+  // rows for the S tiles: one conversion per element instead of eight per 16 DFMA)
+  extern __shared__ __align__(16) float ysm[];
   const int ld = mp + 1;
+  float* stg = ysm + ((YS_RB * ld + 3) & ~3);
+  double* ysd = reinterpret_cast<double*>(stg + 16 * 256);
   const int64_t r0 = (int64_t)blockIdx.x * YS_RB;
   const int cnt = YS_RB * mp;
+  const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(stg + threadIdx.x);
   for (int e0 = threadIdx.x; e0 < cnt; e0 += 4 * 256) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int q0 = 0; q0 < ksplit; q0 += 4) {          // 4 parts × 4 elements = 16 loads in flight
-      float v[4][4];
+    for (int q0 = 0; q0 < ksplit; q0 += 4) {
+      // 4 parts × 4 elements: 16 cp.async into the thread's own staging slots and one wait — in flight together by
+      // construction (as register loads the compiler put every add right behind its load: 16 L2 round trips in a
+      // row, the reason this kernel took 14 µs on C4; clamped addresses, masked at the sum)
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = min(e0 + u * 256, cnt - 1);
+          const int64_t r = min(r0 + e / mp, n - 1);
+          const float* src = Ypart + ((int64_t)min(q0 + qq, ksplit - 1) * n + r) * mp + e % mp;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(st0 + (uint32_t)((qq * 4 + u) * 256 * 4)), "l"(src)
+                       : "memory");
+        }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int e = e0 + u * 256;
-          const int64_t r = r0 + e / mp;
-          v[qq][u] = (q0 + qq < ksplit && e < cnt && r < n) ? Ypart[((int64_t)(q0 + qq) * n + r) * mp + e % mp] : 0.f;
+          const bool ok = q0 + qq < ksplit && e < cnt && r0 + e / mp < n;
+          acc[u] += ok ? stg[(qq * 4 + u) * 256 + threadIdx.x] : 0.f;   // part order unchanged
         }
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] += v[qq][u];            // part order unchanged
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + u * 256;
-      if (e < cnt) ysm[(e / mp) * ld + e % mp] = acc[u];
+      if (e < cnt) {
+        ysm[(e / mp) * ld + e % mp] = acc[u];
+        ysd[(e / mp) * ld + e % mp] = (double)acc[u];
+      }
     }
   }
   __syncthreads();
@@ -687,12 +721,12 @@ __global__ void __launch_bounds__(256) ysum_s_kernel(const float* __restrict__ Y
 #pragma unroll
       for (int v = 0; v < 4; ++v) a[u][v] = 0.0;
     for (int rr = 0; rr < YS_RB; ++rr) {
-      const float* row = ysm + rr * ld;
+      const double* row = ysd + rr * ld;
       double yi[4], yj[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        yi[u] = (double)row[bi * 4 + u];
-        yj[u] = (double)row[bj * 4 + u];
+        yi[u] = row[bi * 4 + u];
+        yj[u] = row[bj * 4 + u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -744,7 +778,7 @@ ppca_status pass_tc_gram(Ctx* c, const ppca_matrix* X, const PassPlan* plan, con
   if (plan->tiles_dev)                          // rows outside the sample stay zero in every part
     PPCA_TRY(check_cuda(c, cudaMemsetAsync(Ypart, 0, (size_t)ksplit * n * mp * sizeof(float), c->stream), "zero Y"));
   PPCA_TRY(run_ka(c, X, Wb, m, mp, S, nullptr, 0, ksplit, Ypart, plan->tiles_dev, plan->ntiles_sel));
-  launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream, Ypart, ksplit, n, mp, m,
+  launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), ysum_s_smem(mp), c->stream, Ypart, ksplit, n, mp, m,
                                                                                             nullptr, 0, Sp);
   PPCA_LAUNCH_CHECK(c, "ysum_s");
   return launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S);
@@ -1135,7 +1169,10 @@ ppca_status pass_tc_power(Ctx* c, const ppca_matrix* X, const PassPlan* plan, co
     const int64_t nb = ceil_div(ldyt, (int64_t)YS_RB);
     double* Sp = (double*)scratch(c, S_NTSTAGE, (size_t)nb * m * m * sizeof(double));
     if (!Sp) return set_error(c, PPCA_ERR_CUDA, "scratch alloc failed");
-    launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), (size_t)YS_RB * (mp + 1) * sizeof(float), c->stream, Ypart, ksplit, n, mp, m,
+    static uint64_t ys_attr = 0;                     // mp = 128: 66 KB of dynamic shared memory
+    if (first_on_device(&ys_attr, c->device))
+      cudaFuncSetAttribute(ysum_s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysum_s_smem(PPCA_MAX_M));
+    launch_pdl(ysum_s_kernel, dim3((unsigned)nb), dim3(256), ysum_s_smem(mp), c->stream, Ypart, ksplit, n, mp, m,
                                                                                               YT, ldyt, Sp);
     PPCA_LAUNCH_CHECK(c, "ysum_s");
     PPCA_TRY(launch_reduce_splits_f64(c, Sp, (int)nb, (int64_t)m * m, S));
